@@ -1,0 +1,83 @@
+"""Build libffspmv.so in-tree for sm_100a.
+
+    python -m paper_1004_3719_b200.build [--force]
+
+CUDA sources are compiled with ``nvcc -gencode arch=compute_100a,code=sm_100a
+-lineinfo -O3``; host sources with g++; everything is linked into
+``paper_1004_3719_b200/libffspmv.so`` with the CUDA runtime linked
+statically.  ptxas register/spill reports go to ``build/ptxas.log``.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(ROOT, "build", "ffspmv")
+LIB = os.path.join(PKG, "libffspmv.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+
+CU_SOURCES = ["kernels.cu", "block.cu", "seq.cu"]
+CPP_SOURCES = ["abi.cpp", "builder.cpp"]
+HEADERS = ["internal.hpp", "device.cuh", "block.cuh"]
+GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return r.stdout + r.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "ffspmv.h")]
+    jobs = []
+    objs = []
+    for s in CU_SOURCES:
+        src = os.path.join(CSRC, s)
+        obj = os.path.join(BUILD, s + ".o")
+        objs.append(obj)
+        if force or _newer(obj, [src] + hdrs):
+            jobs.append([NVCC, "-std=c++17", "-O3", "-lineinfo", *GENCODE, "-Xptxas", "-v",
+                         "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", CSRC,
+                         "-c", src, "-o", obj])
+    for s in CPP_SOURCES:
+        src = os.path.join(CSRC, s)
+        obj = os.path.join(BUILD, s + ".o")
+        objs.append(obj)
+        if force or _newer(obj, [src] + hdrs):
+            jobs.append(["g++", "-std=c++17", "-O3", "-fPIC", "-fvisibility=hidden", "-Wall",
+                         "-I", os.path.join(CUDA, "include"), "-I", CSRC, "-c", src, "-o", obj])
+    logs = []
+    if jobs:
+        with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
+            for out in ex.map(_run, jobs):
+                logs.append(out)
+        with open(os.path.join(BUILD, "ptxas.log"), "a") as f:
+            f.write("\n".join(logs))
+    if force or jobs or _newer(LIB, objs):
+        tmp = LIB + f".tmp{os.getpid()}"
+        _run([NVCC, "-shared", *GENCODE, "-cudart", "static", "-o", tmp, *objs,
+              "-Xlinker", "--exclude-libs,ALL"])
+        os.replace(tmp, LIB)
+    if verbose:
+        print("\n".join(logs))
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,536 @@
+// C ABI (include/ffspmv.h): argument checks, handle lifecycle, device
+// upload, and dispatch to the kernels.  SURVEY §8 row b.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/ffspmv.h"
+#include "internal.hpp"
+
+using namespace ffspmv;
+
+namespace {
+
+thread_local std::string g_err;
+
+ffspmv_status fail(ffspmv_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+ffspmv_status cuda_fail(int e, const char *where) {
+    g_err = std::string(where) + ": " + cudaGetErrorString((cudaError_t)e);
+    return FFSPMV_ERR_CUDA;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev && dev >= 0) {
+            changed = cudaSetDevice(dev) == cudaSuccess;
+        }
+    }
+    ~DeviceGuard() {
+        if (changed) cudaSetDevice(prev);
+    }
+};
+
+struct DevMem {
+    void *base = nullptr;
+    size_t bytes = 0;
+};
+
+bool overlaps(const void *a, size_t an, const void *b, size_t bn) {
+    if (!a || !b || !an || !bn) return false;
+    uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+    return a0 < b0 + bn && b0 < a0 + an;
+}
+
+}  // namespace
+
+struct ffspmv_matrix_s {
+    int device = 0;
+    uint32_t m = 0;
+    DevMod mod{};
+    DevOp op[2]{};         // 0 = A, 1 = A^T
+    bool has_op[2] = {false, false};
+    DevMem mem[2];
+    ffspmv_info info{};
+    uint32_t *flag = nullptr;          // checked-mode flag (device)
+    uint32_t *stage = nullptr;         // apply_host staging (device)
+    size_t stage_elems = 0;
+    bool checked = false;              // check_inputs option
+    std::mutex mu;
+};
+
+namespace {
+
+inline size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// One device allocation per operator; sub-arrays 256 B aligned.
+ffspmv_status upload(const HostOp &h, DevOp &d, DevMem &mem) {
+    struct Part { const void *src; size_t bytes; void **dst; };
+    d = DevOp{};
+    d.rows = h.rows;
+    d.cols = h.cols;
+    d.n_slices = (uint32_t)h.slices.size();
+    d.n_long = (uint32_t)h.longs.size();
+    d.n_groups = (uint32_t)h.groups.size();
+    d.n_split = h.n_split;
+    d.n_zero_rows = (uint32_t)h.zero_rows.size();
+    void *p_slices, *p_perm, *p_pcol, *p_vcol, *p_vval, *p_longs, *p_groups, *p_crow, *p_cpp,
+        *p_cvp, *p_zero, *p_sacc, *p_scnt;
+    Part parts[] = {
+        {h.slices.data(), h.slices.size() * sizeof(SliceHdr), &p_slices},
+        {h.perm.data(), h.perm.size() * 4, &p_perm},
+        {h.pcol.data(), h.pcol.size() * 4, &p_pcol},
+        {h.vcol.data(), h.vcol.size() * 4, &p_vcol},
+        {h.vval.data(), h.vval.size(), &p_vval},
+        {h.longs.data(), h.longs.size() * sizeof(LongItem), &p_longs},
+        {h.groups.data(), h.groups.size() * sizeof(CsrGroup), &p_groups},
+        {h.csr_rows.data(), h.csr_rows.size() * 4, &p_crow},
+        {h.csr_pptr.data(), h.csr_pptr.size() * 4, &p_cpp},
+        {h.csr_vptr.data(), h.csr_vptr.size() * 4, &p_cvp},
+        {h.zero_rows.data(), h.zero_rows.size() * 4, &p_zero},
+        {nullptr, (size_t)h.n_split * 8, &p_sacc},
+        {nullptr, (size_t)h.n_split * 4, &p_scnt},
+    };
+    size_t total = 0;
+    for (auto &pt : parts) total += a256(pt.bytes);
+    total = std::max<size_t>(total, 256);
+    int e = cudaMalloc(&mem.base, total);
+    if (e) return e == cudaErrorMemoryAllocation ? fail(FFSPMV_ERR_NOMEM, "cudaMalloc of matrix")
+                                                 : cuda_fail(e, "cudaMalloc");
+    mem.bytes = total;
+    size_t off = 0;
+    for (auto &pt : parts) {
+        *pt.dst = (char *)mem.base + off;
+        if (pt.bytes) {
+            e = pt.src ? cudaMemcpy(*pt.dst, pt.src, pt.bytes, cudaMemcpyHostToDevice)
+                       : cudaMemset(*pt.dst, 0, pt.bytes);
+            if (e) { cudaFree(mem.base); mem.base = nullptr; return cuda_fail(e, "matrix upload"); }
+        }
+        off += a256(pt.bytes);
+    }
+    d.slices = (const SliceHdr *)p_slices;
+    d.perm = (const uint32_t *)p_perm;
+    d.pcol = (const uint32_t *)p_pcol;
+    d.vcol = (const uint32_t *)p_vcol;
+    d.vval = p_vval;
+    d.longs = (const LongItem *)p_longs;
+    d.groups = (const CsrGroup *)p_groups;
+    d.csr_rows = (const uint32_t *)p_crow;
+    d.csr_pptr = (const uint32_t *)p_cpp;
+    d.csr_vptr = (const uint32_t *)p_cvp;
+    d.zero_rows = (const uint32_t *)p_zero;
+    d.split_acc = (unsigned long long *)p_sacc;
+    d.split_cnt = (uint32_t *)p_scnt;
+    return FFSPMV_OK;
+}
+
+ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &device, bool &want_t,
+                           bool &checked) {
+    device = -1;
+    want_t = true;
+    checked = false;
+    if (!o) return FFSPMV_OK;
+    if (o->struct_size < offsetof(ffspmv_options, dedicated_block))
+        return fail(FFSPMV_ERR_INVALID_ARG, "ffspmv_options.struct_size too small");
+    device = o->device;
+    want_t = o->no_transpose == 0;
+    checked = o->check_inputs != 0;
+    if (o->segregate_pm1 < -1 || o->segregate_pm1 > 1)
+        return fail(FFSPMV_ERR_INVALID_ARG, "segregate_pm1 must be -1, 0 or 1");
+    bo.segregate_pm1 = o->segregate_pm1;
+    if (o->force_format < 0 || o->force_format > 3)
+        return fail(FFSPMV_ERR_INVALID_ARG, "force_format out of range");
+    bo.force_format = o->force_format;
+    if (o->band_rows) {
+        if (o->band_rows % 32) return fail(FFSPMV_ERR_INVALID_ARG, "band_rows must be a multiple of 32");
+        bo.band_rows = o->band_rows;
+    }
+    if (o->long_row) {
+        if (o->long_row > 65535) return fail(FFSPMV_ERR_INVALID_ARG, "long_row must be <= 65535");
+        bo.long_row = o->long_row;
+    }
+    if (o->force_acc_bits && o->force_acc_bits != 32 && o->force_acc_bits != 64 &&
+        o->force_acc_bits != 96)
+        return fail(FFSPMV_ERR_INVALID_ARG, "force_acc_bits must be 0, 32, 64 or 96");
+    bo.force_acc_bits = o->force_acc_bits;
+    if (o->struct_size >= sizeof(ffspmv_options) && o->dedicated_block != 0)
+        return fail(FFSPMV_ERR_INVALID_ARG, "dedicated_block is reserved");
+    return FFSPMV_OK;
+}
+
+ffspmv_status check_triples_args(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t *ri,
+                                 const uint32_t *ci, const int64_t *v, uint32_t m) {
+    if (m < 2) return fail(FFSPMV_ERR_MODULUS, "modulus must be >= 2");
+    if (rows > 0x7FFFFFFFull || cols > 0x7FFFFFFFull)
+        return fail(FFSPMV_ERR_DIM, "rows and cols must be <= 2^31-1");
+    if (nnz >= (1ull << 32)) return fail(FFSPMV_ERR_DIM, "nnz must be < 2^32");
+    if (nnz && (!ri || !ci || !v)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL triple array");
+    return FFSPMV_OK;
+}
+
+void fill_stats(ffspmv_info &I, const HostOp &a, const HostOp *t, uint32_t m) {
+    I.struct_size = sizeof(ffspmv_info);
+    I.modulus = m;
+    I.rows = a.rows;
+    I.cols = a.cols;
+    I.nnz = a.nnz;
+    I.nnz_pm1 = a.nnz_pm;
+    I.nnz_valued = a.nnz_val;
+    I.value_bytes = value_bytes_for(m);
+    I.iterate_bytes = m <= 65536u ? 2 : 4;
+    I.bands = a.bands;
+    I.bands_sell = a.bands_sell;
+    I.bands_csr = a.bands_csr;
+    I.bands_coos = a.bands_coos;
+    I.slices = a.slices.size();
+    I.csr_groups = a.groups.size();
+    I.long_rows = a.long_rows;
+    I.split_rows = a.split_rows;
+    I.padded_slots = a.padded_slots;
+    I.acc_slices_u32 = a.acc_cnt[0];
+    I.acc_slices_u64 = a.acc_cnt[1];
+    I.acc_slices_u96 = a.acc_cnt[2];
+    I.acc_bits_max = a.acc_bits_max;
+    I.stream_bytes = a.stream_bytes;
+    uint64_t vb = I.value_bytes;
+    I.alg_bytes_apply = 4 * a.nnz_pm + (4 + vb) * a.nnz_val + 4ull * a.cols + 4ull * a.rows;
+    if (t)
+        I.alg_bytes_transpose = 4 * t->nnz_pm + (4 + vb) * t->nnz_val + 4ull * t->cols + 4ull * t->rows;
+    I.has_transpose = t != nullptr;
+}
+
+ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t *ri,
+                         const uint32_t *ci, const int64_t *v, uint32_t m, const BuildOptions &bo,
+                         bool want_t, HostOp &A, HostOp &T) {
+    Canon ca;
+    std::string err;
+    int rc;
+    try {
+        rc = canonicalize(ca, rows, cols, nnz, ri, ci, v, m, err);
+    } catch (const std::bad_alloc &) {
+        return fail(FFSPMV_ERR_NOMEM, "host allocation during canonicalisation");
+    }
+    if (rc) return fail((ffspmv_status)rc, err);
+    try {
+        pack_operator(A, ca, m, bo);
+        if (want_t) {
+            Canon ct;
+            transpose_canon(ct, ca);
+            ca = Canon();
+            pack_operator(T, ct, m, bo);
+        }
+    } catch (const std::bad_alloc &) {
+        return fail(FFSPMV_ERR_NOMEM, "host allocation during packing");
+    }
+    if (A.pcol.size() >= (1ull << 32) || A.vcol.size() >= (1ull << 32) ||
+        T.pcol.size() >= (1ull << 32) || T.vcol.size() >= (1ull << 32))
+        return fail(FFSPMV_ERR_DIM, "packed streams exceed 2^32 slots");
+    return FFSPMV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ffspmv_status ffspmv_create(ffspmv_matrix *out, uint64_t rows, uint64_t cols, uint64_t nnz,
+                            const uint32_t *row_idx, const uint32_t *col_idx, const int64_t *vals,
+                            uint32_t modulus, const ffspmv_options *opts) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!out) return fail(FFSPMV_ERR_INVALID_ARG, "out is NULL");
+    ffspmv_status s = check_triples_args(rows, cols, nnz, row_idx, col_idx, vals, modulus);
+    if (s) return s;
+    BuildOptions bo;
+    int device;
+    bool want_t, checked;
+    if ((s = read_options(opts, bo, device, want_t, checked))) return s;
+    if (device < 0) {
+        int e = cudaGetDevice(&device);
+        if (e) return cuda_fail(e, "cudaGetDevice");
+    }
+    int ndev = 0;
+    int e = cudaGetDeviceCount(&ndev);
+    if (e) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device >= ndev) return fail(FFSPMV_ERR_INVALID_ARG, "device ordinal out of range");
+    DeviceGuard guard(device);
+
+    HostOp A, T;
+    if ((s = build_host(rows, cols, nnz, row_idx, col_idx, vals, modulus, bo, want_t, A, T)))
+        return s;
+    ffspmv_matrix h = new (std::nothrow) ffspmv_matrix_s();
+    if (!h) return fail(FFSPMV_ERR_NOMEM, "handle allocation");
+    h->device = device;
+    h->m = modulus;
+    h->mod = make_mod(modulus);
+    if ((s = upload(A, h->op[0], h->mem[0]))) { delete h; return s; }
+    h->has_op[0] = true;
+    if (want_t) {
+        if ((s = upload(T, h->op[1], h->mem[1]))) {
+            cudaFree(h->mem[0].base);
+            delete h;
+            return s;
+        }
+        h->has_op[1] = true;
+    }
+    if ((e = cudaMalloc((void **)&h->flag, 256))) {
+        cudaFree(h->mem[0].base);
+        if (h->mem[1].base) cudaFree(h->mem[1].base);
+        delete h;
+        return cuda_fail(e, "cudaMalloc flag");
+    }
+    fill_stats(h->info, A, want_t ? &T : nullptr, modulus);
+    h->info.nnz_input = nnz;
+    h->info.device_bytes = h->mem[0].bytes + h->mem[1].bytes + 256;
+    h->info.create_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    h->checked = checked;
+    *out = h;
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_destroy(ffspmv_matrix A) {
+    if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    DeviceGuard guard(A->device);
+    for (auto &mem : A->mem)
+        if (mem.base) cudaFree(mem.base);
+    if (A->flag) cudaFree(A->flag);
+    if (A->stage) cudaFree(A->stage);
+    delete A;
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_get_info(ffspmv_matrix A, ffspmv_info *out) {
+    if (!A || !out) return fail(FFSPMV_ERR_INVALID_ARG, "NULL argument");
+    *out = A->info;
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_analyze(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t *row_idx,
+                             const uint32_t *col_idx, const int64_t *vals, uint32_t modulus,
+                             const ffspmv_options *opts, ffspmv_info *info, int transpose,
+                             uint32_t *rec_row, uint32_t *rec_col, uint32_t *rec_val,
+                             uint64_t rec_cap, uint64_t *rec_n) {
+    auto t0 = std::chrono::steady_clock::now();
+    ffspmv_status s = check_triples_args(rows, cols, nnz, row_idx, col_idx, vals, modulus);
+    if (s) return s;
+    BuildOptions bo;
+    int device;
+    bool want_t, checked;
+    if ((s = read_options(opts, bo, device, want_t, checked))) return s;
+    if (transpose) want_t = true;
+    HostOp A, T;
+    if ((s = build_host(rows, cols, nnz, row_idx, col_idx, vals, modulus, bo, want_t, A, T)))
+        return s;
+    if (info) {
+        ffspmv_info I{};
+        fill_stats(I, A, want_t ? &T : nullptr, modulus);
+        I.nnz_input = nnz;
+        I.create_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *info = I;
+    }
+    if (rec_row || rec_col || rec_val) {
+        if (!rec_row || !rec_col || !rec_val || !rec_n)
+            return fail(FFSPMV_ERR_INVALID_ARG, "reconstruction needs all of rec_row/col/val/n");
+        const HostOp &op = transpose ? T : A;
+        uint64_t n = reconstruct(op, modulus, value_bytes_for(modulus), rec_row, rec_col, rec_val,
+                                 rec_cap);
+        *rec_n = n;
+        if (n > rec_cap) return fail(FFSPMV_ERR_NOMEM, "reconstruction capacity too small");
+    }
+    return FFSPMV_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+ffspmv_status check_vec(ffspmv_matrix A, const uint32_t *v, uint64_t n, uint64_t ld, uint64_t w,
+                        void *stream, const char *name) {
+    if (!A->checked || !n || !w) return FFSPMV_OK;
+    int e = cudaMemsetAsync(A->flag, 0, 4, (cudaStream_t)stream);
+    if (!e) e = launch_check_canonical(v, n, ld, w, A->m, A->flag, stream);
+    uint32_t h = 0;
+    if (!e) e = cudaMemcpyAsync(&h, A->flag, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e) return cuda_fail(e, "check_inputs");
+    if (h) return fail(FFSPMV_ERR_INVALID_ARG, std::string(name) + " has an entry >= m");
+    return FFSPMV_OK;
+}
+
+ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_t *x, uint64_t nx,
+                       uint32_t beta, uint32_t *y, uint64_t ny, void *stream) {
+    if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (!A->has_op[which])
+        return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built (no_transpose was set)");
+    const DevOp &op = A->op[which];
+    if (nx != op.cols || ny != op.rows)
+        return fail(FFSPMV_ERR_DIM, "x must have " + std::to_string(op.cols) + " and y " +
+                                        std::to_string(op.rows) + " entries");
+    if ((nx && !x) || (ny && !y)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL vector");
+    if (overlaps(x, nx * 4, y, ny * 4)) return fail(FFSPMV_ERR_INVALID_ARG, "x overlaps y");
+    alpha %= A->m;
+    beta %= A->m;
+    DeviceGuard guard(A->device);
+    ffspmv_status s;
+    if ((s = check_vec(A, x, nx, 1, 1, stream, "x"))) return s;
+    if (beta && (s = check_vec(A, y, ny, 1, 1, stream, "y"))) return s;
+    int e = launch_apply(op, A->mod, alpha, x, beta, y, stream);
+    if (e) return cuda_fail(e, "apply launch");
+    return FFSPMV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ffspmv_status ffspmv_apply(ffspmv_matrix A, uint32_t alpha, const uint32_t *x, uint64_t nx,
+                           uint32_t beta, uint32_t *y, uint64_t ny, void *stream) {
+    return apply_op(A, 0, alpha, x, nx, beta, y, ny, stream);
+}
+
+ffspmv_status ffspmv_apply_transpose(ffspmv_matrix A, uint32_t alpha, const uint32_t *x,
+                                     uint64_t nx, uint32_t beta, uint32_t *y, uint64_t ny,
+                                     void *stream) {
+    return apply_op(A, 1, alpha, x, nx, beta, y, ny, stream);
+}
+
+ffspmv_status ffspmv_apply_block(ffspmv_matrix A, uint32_t k, uint32_t alpha, const uint32_t *X,
+                                 uint64_t ldx, uint32_t beta, uint32_t *Y, uint64_t ldy,
+                                 void *stream) {
+    if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
+    if (ldx < k || ldy < k) return fail(FFSPMV_ERR_INVALID_ARG, "leading dimension < k");
+    const DevOp &op = A->op[0];
+    if ((op.cols && !X) || (op.rows && !Y)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL block");
+    if (overlaps(X, op.cols * ldx * 4, Y, op.rows * ldy * 4))
+        return fail(FFSPMV_ERR_INVALID_ARG, "X overlaps Y");
+    alpha %= A->m;
+    beta %= A->m;
+    DeviceGuard guard(A->device);
+    ffspmv_status s;
+    if ((s = check_vec(A, X, op.cols, ldx, k, stream, "X"))) return s;
+    if (beta && (s = check_vec(A, Y, op.rows, ldy, k, stream, "Y"))) return s;
+    int e = launch_block(op, A->mod, k, alpha, X, ldx, beta, Y, ldy, stream);
+    if (e) return cuda_fail(e, "block launch");
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_apply_host(ffspmv_matrix A, int which, uint32_t alpha, const uint32_t *x_host,
+                                uint32_t beta, uint32_t *y_host, void *stream) {
+    if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (which != FFSPMV_OP_APPLY && which != FFSPMV_OP_TRANSPOSE)
+        return fail(FFSPMV_ERR_INVALID_ARG, "op must be FFSPMV_OP_APPLY or FFSPMV_OP_TRANSPOSE");
+    if (!A->has_op[which]) return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built");
+    const DevOp &op = A->op[which];
+    if ((op.cols && !x_host) || (op.rows && !y_host))
+        return fail(FFSPMV_ERR_INVALID_ARG, "NULL host vector");
+    std::lock_guard<std::mutex> lk(A->mu);
+    DeviceGuard guard(A->device);
+    size_t need = (size_t)op.cols + op.rows;
+    int e;
+    if (need > A->stage_elems) {
+        if (A->stage) cudaFree(A->stage);
+        A->stage = nullptr;
+        A->stage_elems = 0;
+        if ((e = cudaMalloc((void **)&A->stage, std::max<size_t>(need, 1) * 4)))
+            return cuda_fail(e, "cudaMalloc staging");
+        A->stage_elems = need;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *dx = A->stage, *dy = A->stage + op.cols;
+    uint32_t b = beta % A->m;
+    if (op.cols && (e = cudaMemcpyAsync(dx, x_host, op.cols * 4ull, cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "copy x");
+    if (b && op.rows && (e = cudaMemcpyAsync(dy, y_host, op.rows * 4ull, cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "copy y");
+    ffspmv_status s = apply_op(A, which, alpha, dx, op.cols, beta, dy, op.rows, stream);
+    if (s) return s;
+    if (op.rows && (e = cudaMemcpyAsync(y_host, dy, op.rows * 4ull, cudaMemcpyDeviceToHost, st)))
+        return cuda_fail(e, "copy y back");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "synchronize");
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_workspace_size(ffspmv_matrix A, int which, uint32_t k, uint32_t ku,
+                                    size_t *bytes) {
+    if (!A || !bytes) return fail(FFSPMV_ERR_INVALID_ARG, "NULL argument");
+    if (which != FFSPMV_OP_SEQUENCE) { *bytes = 0; return FFSPMV_OK; }
+    if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
+    if (ku == 0) ku = k;
+    DeviceGuard guard(A->device);
+    *bytes = sequence_workspace(A->op[0], A->mod, k, ku);
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_sequence(ffspmv_matrix A, uint32_t k, const uint32_t *X, uint32_t ku,
+                              const uint32_t *U, uint64_t L, uint32_t *S, uint32_t *V_out,
+                              void *workspace, size_t workspace_bytes, void *stream) {
+    if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    const DevOp &op = A->op[0];
+    if (op.rows != op.cols) return fail(FFSPMV_ERR_NONSQUARE, "sequence needs a square matrix");
+    if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
+    if (!U) {
+        if (ku != 0 && ku != k) return fail(FFSPMV_ERR_INVALID_ARG, "U == NULL requires ku == k");
+        ku = k;
+    } else if (ku == 0) {
+        return fail(FFSPMV_ERR_INVALID_ARG, "ku must be >= 1");
+    }
+    const uint64_t n = op.rows;
+    if (n && !X) return fail(FFSPMV_ERR_INVALID_ARG, "NULL X");
+    if (L && !S) return fail(FFSPMV_ERR_INVALID_ARG, "NULL S");
+    if (overlaps(S, L * ku * k * 4ull, X, n * k * 4ull) ||
+        overlaps(V_out, n * k * 4ull, X, n * k * 4ull) ||
+        overlaps(V_out, n * k * 4ull, S, L * ku * k * 4ull) ||
+        overlaps(S, L * ku * k * 4ull, U, n * ku * 4ull))
+        return fail(FFSPMV_ERR_INVALID_ARG, "S / V_out overlap an input");
+    DeviceGuard guard(A->device);
+    size_t need = sequence_workspace(op, A->mod, k, ku);
+    if (n && (!workspace || workspace_bytes < need))
+        return fail(FFSPMV_ERR_NOMEM, "workspace smaller than ffspmv_workspace_size (" +
+                                          std::to_string(need) + " bytes)");
+    ffspmv_status s;
+    if ((s = check_vec(A, X, n, k, k, stream, "X"))) return s;
+    if (U && (s = check_vec(A, U, n, ku, ku, stream, "U"))) return s;
+    if (n == 0) {
+        if (L && (S)) {
+            int e = cudaMemsetAsync(S, 0, L * ku * k * 4ull, (cudaStream_t)stream);
+            if (e) return cuda_fail(e, "memset S");
+        }
+        return FFSPMV_OK;
+    }
+    int e = launch_sequence(op, A->mod, k, X, ku, U, L, S, V_out, workspace, workspace_bytes, stream);
+    if (e) return cuda_fail(e, "sequence launch");
+    return FFSPMV_OK;
+}
+
+const char *ffspmv_status_string(ffspmv_status s) {
+    switch (s) {
+        case FFSPMV_OK: return "FFSPMV_OK";
+        case FFSPMV_ERR_INVALID_ARG: return "FFSPMV_ERR_INVALID_ARG";
+        case FFSPMV_ERR_MODULUS: return "FFSPMV_ERR_MODULUS";
+        case FFSPMV_ERR_INDEX: return "FFSPMV_ERR_INDEX";
+        case FFSPMV_ERR_DIM: return "FFSPMV_ERR_DIM";
+        case FFSPMV_ERR_NONSQUARE: return "FFSPMV_ERR_NONSQUARE";
+        case FFSPMV_ERR_UNSUPPORTED: return "FFSPMV_ERR_UNSUPPORTED";
+        case FFSPMV_ERR_NOMEM: return "FFSPMV_ERR_NOMEM";
+        case FFSPMV_ERR_CUDA: return "FFSPMV_ERR_CUDA";
+        case FFSPMV_ERR_NCCL: return "FFSPMV_ERR_NCCL";
+    }
+    return "FFSPMV_ERR_UNKNOWN";
+}
+
+const char *ffspmv_last_error(void) { return g_err.c_str(); }
+
+int ffspmv_version(void) { return 100; }
+
+uint64_t ffspmv_kernel_launches(void) { return kernel_launch_count(); }
+
+}  // extern "C"

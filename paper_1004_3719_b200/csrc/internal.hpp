@@ -1,0 +1,153 @@
+// Internal layout shared by the host builder (builder.cpp), the C ABI
+// (abi.cpp) and the CUDA kernels (kernels.cu).  Nothing here is part of the
+// public ABI (include/ffspmv.h).  See DESIGN.md §"Data layout in HBM".
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ffspmv {
+
+// A slot whose column is PAD_COL contributes nothing (ELL padding).
+// Valid columns are < 2^31 - 1, so the sentinel never collides.
+constexpr uint32_t PAD_COL = 0x7FFFFFFFu;
+// Bit 31 of an index-only (+-1) slot is the sign: set = "-1".
+constexpr uint32_t SIGN_BIT = 0x80000000u;
+constexpr uint32_t COL_MASK = 0x7FFFFFFFu;
+constexpr uint32_t PAD_ROW = 0xFFFFFFFFu;
+constexpr uint32_t NO_SPLIT = 0xFFFFFFFFu;
+
+// Accumulator width (P:129-147 delayed reduction with integer carriers).
+enum Regime : uint8_t { ACC32 = 0, ACC64 = 1, ACC96 = 2 };
+
+// One 32-row slice of a SELL band.  Slot j of lane l lives at
+// off + j*32 + l in its stream (column-major inside the slice).
+struct SliceHdr {
+    uint32_t off_p;   // element offset of the +-1 stream slots
+    uint32_t off_v;   // element offset of the valued stream slots (cols + vals)
+    uint16_t wp;      // +-1 slots per lane
+    uint16_t wv;      // valued slots per lane
+    uint8_t regime;   // Regime
+    uint8_t nrows;    // live lanes (rows) in the slice
+    uint16_t band;    // band index (diagnostics)
+};
+static_assert(sizeof(SliceHdr) == 16, "SliceHdr is 16 bytes");
+
+// A long row (or one chunk of a split long row) of the COO/CSR tail.
+// Chunks of one row are consecutive in the long-item array.
+struct LongItem {
+    uint32_t row;
+    uint32_t off_p, len_p;   // +-1 entries of this chunk
+    uint32_t off_v, len_v;   // valued entries of this chunk
+    uint32_t split;          // NO_SPLIT, or index of the split-row scratch cell
+    uint32_t chunk;          // chunk index inside the row
+    uint32_t nch_reg;        // nchunks | regime << 28 (regime of one lane's share)
+};
+static_assert(sizeof(LongItem) == 32, "LongItem is 32 bytes");
+
+// A warp's worth of rows of a CSR-vector or COO_S band: V = 1 << vlog lanes
+// per row, 32 >> vlog rows per warp pass.  Rows are listed in csr_rows
+// (natural order for CSR, non-empty rows only for COO_S); listed row i owns
+// +-1 entries [csr_pptr[i], csr_pptr[i+1]) and valued entries
+// [csr_vptr[i], csr_vptr[i+1]).
+struct CsrGroup {
+    uint32_t first;   // index of the first listed row
+    uint16_t nrows;   // listed rows in this group (<= 32)
+    uint8_t vlog;     // log2 lanes per row
+    uint8_t regime;
+    uint32_t band;
+    uint32_t pad_;
+};
+static_assert(sizeof(CsrGroup) == 16, "CsrGroup is 16 bytes");
+
+// Modulus constants for Barrett reduction of u64 / u96 sums.
+struct DevMod {
+    uint32_t m;
+    uint32_t vbytes;     // bytes per stored value (1, 2, 4)
+    uint64_t mu;         // floor(2^64 / m)
+    uint64_t r64;        // 2^64 mod m
+};
+
+// Device view of one packed operator (A or A^T).
+struct DevOp {
+    uint32_t rows, cols;
+    uint32_t n_slices, n_long, n_groups, n_split;
+    uint32_t n_zero_rows;          // rows of COO_S bands with no entries
+    const SliceHdr *slices;
+    const uint32_t *perm;          // slice lane -> row (PAD_ROW for dead lanes)
+    const uint32_t *pcol;          // +-1 stream: col | sign, PAD_COL pads
+    const uint32_t *vcol;          // valued stream: col, PAD_COL pads
+    const void *vval;              // values (vbytes each), 0 for pads
+    const LongItem *longs;
+    const CsrGroup *groups;
+    const uint32_t *csr_rows, *csr_pptr, *csr_vptr;
+    const uint32_t *zero_rows;     // rows written as beta*y only
+    unsigned long long *split_acc; // per split row: sum of chunk residues
+    uint32_t *split_cnt;           // per split row: chunks arrived
+};
+
+// Host-side packed operator.
+struct HostOp {
+    uint32_t rows = 0, cols = 0;
+    std::vector<SliceHdr> slices;
+    std::vector<uint32_t> perm;
+    std::vector<uint32_t> pcol, vcol;
+    std::vector<uint8_t> vval;       // vbytes per element
+    std::vector<LongItem> longs;
+    uint32_t n_split = 0;
+    std::vector<CsrGroup> groups;
+    std::vector<uint32_t> csr_rows, csr_pptr, csr_vptr;
+    std::vector<uint32_t> zero_rows;
+    // statistics
+    uint64_t nnz = 0, nnz_pm = 0, nnz_val = 0;
+    uint32_t bands = 0, bands_sell = 0, bands_csr = 0, bands_coos = 0;
+    uint64_t long_rows = 0, split_rows = 0, padded_slots = 0;
+    uint32_t acc_cnt[3] = {0, 0, 0};
+    uint32_t acc_bits_max = 32;
+    uint64_t stream_bytes = 0;
+};
+
+struct BuildOptions {
+    int segregate_pm1 = 0;     // 0 auto, 1 on, -1 off
+    int force_format = 0;
+    uint32_t band_rows = 4096;
+    uint32_t long_row = 512;
+    uint32_t split_chunk = 1u << 14;
+    int force_acc_bits = 0;
+};
+
+// Canonical CSR: rows sorted by column, duplicates summed mod m, zeros dropped.
+struct Canon {
+    uint64_t nrows = 0, ncols = 0;
+    std::vector<uint64_t> ptr;
+    std::vector<uint32_t> idx;
+    std::vector<uint32_t> val;   // residues in [1, m-1]
+};
+
+// builder.cpp
+int canonicalize(Canon &out, uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t *ri,
+                 const uint32_t *ci, const int64_t *v, uint32_t m, std::string &err);
+void transpose_canon(Canon &out, const Canon &a);
+void pack_operator(HostOp &op, const Canon &a, uint32_t m, const BuildOptions &bo);
+uint64_t reconstruct(const HostOp &op, uint32_t m, uint32_t vbytes, uint32_t *rr, uint32_t *rc,
+                     uint32_t *rv, uint64_t cap);
+uint32_t value_bytes_for(uint32_t m);
+DevMod make_mod(uint32_t m);
+
+// kernels.cu launchers (return cudaError_t as int)
+int launch_apply(const DevOp &op, const DevMod &M, uint32_t alpha, const uint32_t *x,
+                 uint32_t beta, uint32_t *y, void *stream);
+int launch_block(const DevOp &op, const DevMod &M, uint32_t k, uint32_t alpha,
+                 const uint32_t *X, uint64_t ldx, uint32_t beta, uint32_t *Y, uint64_t ldy,
+                 void *stream);
+size_t sequence_workspace(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku);
+int launch_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X,
+                    uint32_t ku, const uint32_t *U, uint64_t L, uint32_t *S, uint32_t *V_out,
+                    void *ws, size_t ws_bytes, void *stream);
+int launch_check_canonical(const uint32_t *v, uint64_t n, uint64_t ld, uint64_t w, uint32_t m,
+                           uint32_t *flag_dev, void *stream);
+uint64_t kernel_launch_count();
+
+}  // namespace ffspmv
