@@ -11,10 +11,18 @@ __global__ void k_rows(const uint32_t* __restrict__ idx, const uint32_t* __restr
     const uint32_t lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
     uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t i = warp * (32 / G) + sub; i < nrows_g; i += nw * (32 / G)) {
-        uint32_t r = __ldg(idx + i);
-        acc += __ldg(X + (uint64_t)r * G + sl);
+    const uint64_t stride = nw * (32 / G);
+    uint64_t i = warp * (32 / G) + sub;
+    for (; i + 7 * stride < nrows_g; i += 8 * stride) {
+        uint32_t r[8], v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = __ldg(idx + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (uint64_t)r[u] * G + sl);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
     }
+    for (; i < nrows_g; i += stride) acc += __ldg(X + (uint64_t)__ldg(idx + i) * G + sl);
     if (acc == 0x12345678) out[0] = acc;
 }
 
