@@ -22,9 +22,10 @@
  *     passed as void*; NULL = the legacy default stream).  Argument errors
  *     return immediately; device faults surface at the caller's next sync.
  *   - A handle is immutable after create: calls on distinct outputs may run
- *     concurrently, except that a matrix with split rows (info.split_rows > 0,
- *     rows longer than 2^14 nonzeros) uses an internal scratch in apply /
- *     apply_transpose, so those calls on one handle must be stream-ordered.
+ *     concurrently, except that apply / apply_transpose use an internal
+ *     scratch when the operator uses PANELS (info.strategy_* == PANELS) or has
+ *     split rows (info.split_rows > 0): those calls on one handle must then be
+ *     ordered on one stream.
  *   - On error a status is returned (never an abort), out-parameters are
  *     untouched, and ffspmv_last_error() holds a thread-local message.
  */
@@ -75,6 +76,15 @@ enum {
                                                                       */
 };
 
+/* Layout of the k = 1 products (apply, apply_transpose).  ROWS: the band
+ * formats above, x gathered from L2 per nonzero.  PANELS: A cut into column
+ * panels x row bands (the column-wise split of P:290-295); each tile stages
+ * its slice of x in shared memory and accumulates its band rows there, then a
+ * reduction pass sums the panels (Fig. 2).  AUTO picks PANELS when
+ * the columns show little locality (random gathers would be L2-bound).
+ * Block apply and the sequence always use ROWS. */
+enum { FFSPMV_STRATEGY_AUTO = 0, FFSPMV_STRATEGY_ROWS = 1, FFSPMV_STRATEGY_PANELS = 2 };
+
 /* Operation selectors for ffspmv_apply_host / ffspmv_workspace_size. */
 enum { FFSPMV_OP_APPLY = 0, FFSPMV_OP_TRANSPOSE = 1, FFSPMV_OP_BLOCK = 2, FFSPMV_OP_SEQUENCE = 3 };
 
@@ -99,7 +109,9 @@ typedef struct {
                                 width (testing: results must not change)         */
     int32_t check_inputs;    /* 1: apply/sequence verify that x / X / U / y are
                                 canonical (one extra pass + sync per call)       */
-    int32_t dedicated_block; /* reserved, must be 0                               */
+    int32_t strategy;        /* apply / apply_transpose layout: FFSPMV_STRATEGY_* */
+    uint32_t panel_rows;     /* PANELS: rows per band, 0 = default (testing)      */
+    uint32_t panel_cols;     /* PANELS: columns per panel, 0 = default (testing)  */
 } ffspmv_options;
 
 /* Summary of a built (or analysed) matrix. */
@@ -130,6 +142,11 @@ typedef struct {
     uint64_t alg_bytes_transpose;
     uint32_t has_transpose;
     double create_seconds;
+    uint32_t strategy_apply;      /* FFSPMV_STRATEGY_ROWS or _PANELS actually used */
+    uint32_t strategy_transpose;
+    uint32_t panels, panel_bands; /* P and B of the apply operator (PANELS)       */
+    uint64_t panel_stream_bytes;  /* packed bytes read by one PANELS apply         */
+    double gather_locality;       /* distinct 128 B x lines / nonzeros (sampled)   */
 } ffspmv_info;
 
 /* --- lifecycle ------------------------------------------------------------ */

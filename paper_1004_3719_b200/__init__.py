@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libffspmv.so")
 OK, ERR_INVALID_ARG, ERR_MODULUS, ERR_INDEX, ERR_DIM, ERR_NONSQUARE, ERR_UNSUPPORTED, \
     ERR_NOMEM, ERR_CUDA, ERR_NCCL = range(10)
 FMT_AUTO, FMT_SELL, FMT_CSR, FMT_COOS = range(4)
+STRATEGY_AUTO, STRATEGY_ROWS, STRATEGY_PANELS = range(3)
 OP_APPLY, OP_TRANSPOSE, OP_BLOCK, OP_SEQUENCE = range(4)
 
 # Every symbol include/ffspmv.h declares (checked by tests/test_abi.py).
@@ -43,7 +44,9 @@ class ffspmv_options(ctypes.Structure):
         ("long_row", ctypes.c_uint32),
         ("force_acc_bits", ctypes.c_int32),
         ("check_inputs", ctypes.c_int32),
-        ("dedicated_block", ctypes.c_int32),
+        ("strategy", ctypes.c_int32),
+        ("panel_rows", ctypes.c_uint32),
+        ("panel_cols", ctypes.c_uint32),
     ]
 
 
@@ -78,6 +81,12 @@ class ffspmv_info(ctypes.Structure):
         ("alg_bytes_transpose", ctypes.c_uint64),
         ("has_transpose", ctypes.c_uint32),
         ("create_seconds", ctypes.c_double),
+        ("strategy_apply", ctypes.c_uint32),
+        ("strategy_transpose", ctypes.c_uint32),
+        ("panels", ctypes.c_uint32),
+        ("panel_bands", ctypes.c_uint32),
+        ("panel_stream_bytes", ctypes.c_uint64),
+        ("gather_locality", ctypes.c_double),
     ]
 
 
@@ -153,7 +162,8 @@ def _check(rc):
 
 
 def make_options(device=-1, no_transpose=False, segregate_pm1=0, force_format=FMT_AUTO,
-                 band_rows=0, long_row=0, force_acc_bits=0, check_inputs=False):
+                 band_rows=0, long_row=0, force_acc_bits=0, check_inputs=False,
+                 strategy=STRATEGY_AUTO, panel_rows=0, panel_cols=0):
     o = ffspmv_options()
     o.struct_size = ctypes.sizeof(ffspmv_options)
     o.device = device
@@ -164,6 +174,9 @@ def make_options(device=-1, no_transpose=False, segregate_pm1=0, force_format=FM
     o.long_row = long_row
     o.force_acc_bits = force_acc_bits
     o.check_inputs = int(bool(check_inputs))
+    o.strategy = strategy
+    o.panel_rows = panel_rows
+    o.panel_cols = panel_cols
     return o
 
 

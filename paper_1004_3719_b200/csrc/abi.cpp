@@ -56,9 +56,12 @@ struct ffspmv_matrix_s {
     int device = 0;
     uint32_t m = 0;
     DevMod mod{};
-    DevOp op[2]{};         // 0 = A, 1 = A^T
+    DevOp op[2]{};         // 0 = A, 1 = A^T: row layout
     bool has_op[2] = {false, false};
     DevMem mem[2];
+    DevPanel pan[2]{};     // 0 = A, 1 = A^T: panel layout (k = 1 products)
+    bool has_pan[2] = {false, false};
+    DevMem pmem[2];
     ffspmv_info info{};
     uint32_t *flag = nullptr;          // checked-mode flag (device)
     uint32_t *stage = nullptr;         // apply_host staging (device)
@@ -132,13 +135,55 @@ ffspmv_status upload(const HostOp &h, DevOp &d, DevMem &mem) {
     return FFSPMV_OK;
 }
 
+ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
+    struct Part { const void *src; size_t bytes; void **dst; };
+    d = DevPanel{};
+    d.rows = h.rows;
+    d.cols = h.cols;
+    d.g = h.g;
+    void *p_tp, *p_tv, *p_pent, *p_vent, *p_vval, *p_cta, *p_part;
+    Part parts[] = {
+        {h.tp.data(), h.tp.size() * 4, &p_tp},
+        {h.tv.data(), h.tv.size() * 4, &p_tv},
+        {h.pent.data(), h.pent.size() * 4, &p_pent},
+        {h.vent.data(), h.vent.size() * 4, &p_vent},
+        {h.vval.data(), h.vval.size(), &p_vval},
+        {h.cta_t0.data(), h.cta_t0.size() * 4, &p_cta},
+        {nullptr, (size_t)h.g.P * h.rows * h.g.xbytes, &p_part},
+    };
+    size_t total = 0;
+    for (auto &pt : parts) total += a256(pt.bytes);
+    total = std::max<size_t>(total, 256);
+    int e = cudaMalloc(&mem.base, total);
+    if (e) return e == cudaErrorMemoryAllocation ? fail(FFSPMV_ERR_NOMEM, "cudaMalloc of panels")
+                                                 : cuda_fail(e, "cudaMalloc");
+    mem.bytes = total;
+    size_t off = 0;
+    for (auto &pt : parts) {
+        *pt.dst = (char *)mem.base + off;
+        if (pt.bytes && pt.src) {
+            e = cudaMemcpy(*pt.dst, pt.src, pt.bytes, cudaMemcpyHostToDevice);
+            if (e) { cudaFree(mem.base); mem.base = nullptr; return cuda_fail(e, "panel upload"); }
+        }
+        off += a256(pt.bytes);
+    }
+    d.tp = (const uint32_t *)p_tp;
+    d.tv = (const uint32_t *)p_tv;
+    d.pent = (const uint32_t *)p_pent;
+    d.vent = (const uint32_t *)p_vent;
+    d.vval = p_vval;
+    d.cta_t0 = (const uint32_t *)p_cta;
+    d.partial = p_part;
+    return FFSPMV_OK;
+}
+
 ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &device, bool &want_t,
                            bool &checked) {
     device = -1;
     want_t = true;
     checked = false;
     if (!o) return FFSPMV_OK;
-    if (o->struct_size < offsetof(ffspmv_options, dedicated_block))
+    if (o->struct_size < offsetof(ffspmv_options, strategy))
         return fail(FFSPMV_ERR_INVALID_ARG, "ffspmv_options.struct_size too small");
     device = o->device;
     want_t = o->no_transpose == 0;
@@ -161,8 +206,17 @@ ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &devic
         o->force_acc_bits != 96)
         return fail(FFSPMV_ERR_INVALID_ARG, "force_acc_bits must be 0, 32, 64 or 96");
     bo.force_acc_bits = o->force_acc_bits;
-    if (o->struct_size >= sizeof(ffspmv_options) && o->dedicated_block != 0)
-        return fail(FFSPMV_ERR_INVALID_ARG, "dedicated_block is reserved");
+    if (o->struct_size >= sizeof(ffspmv_options)) {
+        if (o->strategy < 0 || o->strategy > 2)
+            return fail(FFSPMV_ERR_INVALID_ARG, "strategy must be 0, 1 or 2");
+        bo.strategy = o->strategy;
+        if (o->panel_rows && (o->panel_rows > 16384 || o->panel_rows % 32))
+            return fail(FFSPMV_ERR_INVALID_ARG, "panel_rows must be a multiple of 32 <= 16384");
+        if (o->panel_cols && (o->panel_cols > 65536 || o->panel_cols % 32))
+            return fail(FFSPMV_ERR_INVALID_ARG, "panel_cols must be a multiple of 32 <= 65536");
+        bo.panel_rows = o->panel_rows;
+        bo.panel_cols = o->panel_cols;
+    }
     return FFSPMV_OK;
 }
 
@@ -176,7 +230,16 @@ ffspmv_status check_triples_args(uint64_t rows, uint64_t cols, uint64_t nnz, con
     return FFSPMV_OK;
 }
 
-void fill_stats(ffspmv_info &I, const HostOp &a, const HostOp *t, uint32_t m) {
+struct Built {
+    HostOp rows[2];
+    HostPanel pan[2];
+    bool has_rows[2] = {false, false};
+    bool has_pan[2] = {false, false};
+    double locality = 0;
+};
+
+void fill_stats(ffspmv_info &I, const Built &b, uint32_t m) {
+    const HostOp &a = b.rows[0];
     I.struct_size = sizeof(ffspmv_info);
     I.modulus = m;
     I.rows = a.rows;
@@ -202,14 +265,31 @@ void fill_stats(ffspmv_info &I, const HostOp &a, const HostOp *t, uint32_t m) {
     I.stream_bytes = a.stream_bytes;
     uint64_t vb = I.value_bytes;
     I.alg_bytes_apply = 4 * a.nnz_pm + (4 + vb) * a.nnz_val + 4ull * a.cols + 4ull * a.rows;
-    if (t)
-        I.alg_bytes_transpose = 4 * t->nnz_pm + (4 + vb) * t->nnz_val + 4ull * t->cols + 4ull * t->rows;
-    I.has_transpose = t != nullptr;
+    bool has_t = b.has_rows[1] || b.has_pan[1];
+    if (has_t)
+        I.alg_bytes_transpose = 4 * a.nnz_pm + (4 + vb) * a.nnz_val + 4ull * a.cols + 4ull * a.rows;
+    I.has_transpose = has_t;
+    I.strategy_apply = b.has_pan[0] ? FFSPMV_STRATEGY_PANELS : FFSPMV_STRATEGY_ROWS;
+    I.strategy_transpose = !has_t ? 0 : b.has_pan[1] ? FFSPMV_STRATEGY_PANELS : FFSPMV_STRATEGY_ROWS;
+    if (b.has_pan[0]) {
+        I.panels = b.pan[0].g.P;
+        I.panel_bands = b.pan[0].g.B;
+        I.panel_stream_bytes = b.pan[0].stream_bytes;
+    }
+    I.gather_locality = b.locality;
+}
+
+bool choose_panels(const Canon &c, uint32_t m, const BuildOptions &bo, uint32_t nsm, double loc) {
+    if (bo.strategy == FFSPMV_STRATEGY_ROWS) return false;
+    if (bo.strategy == FFSPMV_STRATEGY_PANELS) return true;
+    PanelGeom g = panel_geometry(c.nrows, c.ncols, m, bo, nsm);
+    // random columns (little line reuse) + enough tiles to fill the SMs
+    return loc > 0.5 && (uint64_t)g.P * g.B >= nsm && c.idx.size() >= (1u << 20);
 }
 
 ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t *ri,
                          const uint32_t *ci, const int64_t *v, uint32_t m, const BuildOptions &bo,
-                         bool want_t, HostOp &A, HostOp &T) {
+                         bool want_t, uint32_t nsm, Built &out) {
     Canon ca;
     std::string err;
     int rc;
@@ -220,20 +300,40 @@ ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint3
     }
     if (rc) return fail((ffspmv_status)rc, err);
     try {
-        pack_operator(A, ca, m, bo);
+        out.locality = gather_locality(ca);
+        pack_operator(out.rows[0], ca, m, bo);   // block apply + sequence always use rows
+        out.has_rows[0] = true;
+        if (choose_panels(ca, m, bo, nsm, out.locality)) {
+            pack_panels(out.pan[0], ca, m, bo, nsm);
+            out.has_pan[0] = true;
+        }
         if (want_t) {
             Canon ct;
             transpose_canon(ct, ca);
             ca = Canon();
-            pack_operator(T, ct, m, bo);
+            if (choose_panels(ct, m, bo, nsm, gather_locality(ct))) {
+                pack_panels(out.pan[1], ct, m, bo, nsm);
+                out.has_pan[1] = true;
+            } else {
+                pack_operator(out.rows[1], ct, m, bo);
+                out.has_rows[1] = true;
+            }
         }
     } catch (const std::bad_alloc &) {
         return fail(FFSPMV_ERR_NOMEM, "host allocation during packing");
     }
-    if (A.pcol.size() >= (1ull << 32) || A.vcol.size() >= (1ull << 32) ||
-        T.pcol.size() >= (1ull << 32) || T.vcol.size() >= (1ull << 32))
-        return fail(FFSPMV_ERR_DIM, "packed streams exceed 2^32 slots");
+    for (int k = 0; k < 2; ++k)
+        if (out.rows[k].pcol.size() >= (1ull << 32) || out.rows[k].vcol.size() >= (1ull << 32) ||
+            out.pan[k].pent.size() >= (1ull << 32) || out.pan[k].vent.size() >= (1ull << 32))
+            return fail(FFSPMV_ERR_DIM, "packed streams exceed 2^32 slots");
     return FFSPMV_OK;
+}
+
+uint32_t device_sms(int device) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0)
+        n = 148;
+    return (uint32_t)n;
 }
 
 }  // namespace
@@ -261,33 +361,40 @@ ffspmv_status ffspmv_create(ffspmv_matrix *out, uint64_t rows, uint64_t cols, ui
     if (device >= ndev) return fail(FFSPMV_ERR_INVALID_ARG, "device ordinal out of range");
     DeviceGuard guard(device);
 
-    HostOp A, T;
-    if ((s = build_host(rows, cols, nnz, row_idx, col_idx, vals, modulus, bo, want_t, A, T)))
+    Built B;
+    if ((s = build_host(rows, cols, nnz, row_idx, col_idx, vals, modulus, bo, want_t,
+                        device_sms(device), B)))
         return s;
     ffspmv_matrix h = new (std::nothrow) ffspmv_matrix_s();
     if (!h) return fail(FFSPMV_ERR_NOMEM, "handle allocation");
     h->device = device;
     h->m = modulus;
     h->mod = make_mod(modulus);
-    if ((s = upload(A, h->op[0], h->mem[0]))) { delete h; return s; }
-    h->has_op[0] = true;
-    if (want_t) {
-        if ((s = upload(T, h->op[1], h->mem[1]))) {
-            cudaFree(h->mem[0].base);
-            delete h;
-            return s;
+    auto cleanup = [&]() {
+        for (int k = 0; k < 2; ++k) {
+            if (h->mem[k].base) cudaFree(h->mem[k].base);
+            if (h->pmem[k].base) cudaFree(h->pmem[k].base);
         }
-        h->has_op[1] = true;
+        if (h->flag) cudaFree(h->flag);
+        delete h;
+    };
+    for (int k = 0; k < 2; ++k) {
+        if (B.has_rows[k]) {
+            if ((s = upload(B.rows[k], h->op[k], h->mem[k]))) { cleanup(); return s; }
+            h->has_op[k] = true;
+        }
+        if (B.has_pan[k]) {
+            if ((s = upload_panel(B.pan[k], h->pan[k], h->pmem[k]))) { cleanup(); return s; }
+            h->has_pan[k] = true;
+        }
     }
     if ((e = cudaMalloc((void **)&h->flag, 256))) {
-        cudaFree(h->mem[0].base);
-        if (h->mem[1].base) cudaFree(h->mem[1].base);
-        delete h;
+        cleanup();
         return cuda_fail(e, "cudaMalloc flag");
     }
-    fill_stats(h->info, A, want_t ? &T : nullptr, modulus);
+    fill_stats(h->info, B, modulus);
     h->info.nnz_input = nnz;
-    h->info.device_bytes = h->mem[0].bytes + h->mem[1].bytes + 256;
+    h->info.device_bytes = h->mem[0].bytes + h->mem[1].bytes + h->pmem[0].bytes + h->pmem[1].bytes + 256;
     h->info.create_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     h->checked = checked;
@@ -299,6 +406,8 @@ ffspmv_status ffspmv_destroy(ffspmv_matrix A) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
     DeviceGuard guard(A->device);
     for (auto &mem : A->mem)
+        if (mem.base) cudaFree(mem.base);
+    for (auto &mem : A->pmem)
         if (mem.base) cudaFree(mem.base);
     if (A->flag) cudaFree(A->flag);
     if (A->stage) cudaFree(A->stage);
@@ -325,12 +434,12 @@ ffspmv_status ffspmv_analyze(uint64_t rows, uint64_t cols, uint64_t nnz, const u
     bool want_t, checked;
     if ((s = read_options(opts, bo, device, want_t, checked))) return s;
     if (transpose) want_t = true;
-    HostOp A, T;
-    if ((s = build_host(rows, cols, nnz, row_idx, col_idx, vals, modulus, bo, want_t, A, T)))
+    Built B;
+    if ((s = build_host(rows, cols, nnz, row_idx, col_idx, vals, modulus, bo, want_t, 148, B)))
         return s;
     if (info) {
         ffspmv_info I{};
-        fill_stats(I, A, want_t ? &T : nullptr, modulus);
+        fill_stats(I, B, modulus);
         I.nnz_input = nnz;
         I.create_seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -339,9 +448,12 @@ ffspmv_status ffspmv_analyze(uint64_t rows, uint64_t cols, uint64_t nnz, const u
     if (rec_row || rec_col || rec_val) {
         if (!rec_row || !rec_col || !rec_val || !rec_n)
             return fail(FFSPMV_ERR_INVALID_ARG, "reconstruction needs all of rec_row/col/val/n");
-        const HostOp &op = transpose ? T : A;
-        uint64_t n = reconstruct(op, modulus, value_bytes_for(modulus), rec_row, rec_col, rec_val,
-                                 rec_cap);
+        const int k = transpose ? 1 : 0;
+        uint64_t n = B.has_pan[k]
+                         ? reconstruct_panels(B.pan[k], modulus, value_bytes_for(modulus), rec_row,
+                                              rec_col, rec_val, rec_cap)
+                         : reconstruct(B.rows[k], modulus, value_bytes_for(modulus), rec_row,
+                                       rec_col, rec_val, rec_cap);
         *rec_n = n;
         if (n > rec_cap) return fail(FFSPMV_ERR_NOMEM, "reconstruction capacity too small");
     }
@@ -368,12 +480,13 @@ ffspmv_status check_vec(ffspmv_matrix A, const uint32_t *v, uint64_t n, uint64_t
 ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_t *x, uint64_t nx,
                        uint32_t beta, uint32_t *y, uint64_t ny, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
-    if (!A->has_op[which])
+    if (!A->has_op[which] && !A->has_pan[which])
         return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built (no_transpose was set)");
-    const DevOp &op = A->op[which];
-    if (nx != op.cols || ny != op.rows)
-        return fail(FFSPMV_ERR_DIM, "x must have " + std::to_string(op.cols) + " and y " +
-                                        std::to_string(op.rows) + " entries");
+    const uint64_t orows = A->has_pan[which] ? A->pan[which].rows : A->op[which].rows;
+    const uint64_t ocols = A->has_pan[which] ? A->pan[which].cols : A->op[which].cols;
+    if (nx != ocols || ny != orows)
+        return fail(FFSPMV_ERR_DIM, "x must have " + std::to_string(ocols) + " and y " +
+                                        std::to_string(orows) + " entries");
     if ((nx && !x) || (ny && !y)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL vector");
     if (overlaps(x, nx * 4, y, ny * 4)) return fail(FFSPMV_ERR_INVALID_ARG, "x overlaps y");
     alpha %= A->m;
@@ -382,7 +495,8 @@ ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_
     ffspmv_status s;
     if ((s = check_vec(A, x, nx, 1, 1, stream, "x"))) return s;
     if (beta && (s = check_vec(A, y, ny, 1, 1, stream, "y"))) return s;
-    int e = launch_apply(op, A->mod, alpha, x, beta, y, stream);
+    int e = A->has_pan[which] ? launch_panel_apply(A->pan[which], A->mod, alpha, x, beta, y, stream)
+                              : launch_apply(A->op[which], A->mod, alpha, x, beta, y, stream);
     if (e) return cuda_fail(e, "apply launch");
     return FFSPMV_OK;
 }
@@ -428,8 +542,10 @@ ffspmv_status ffspmv_apply_host(ffspmv_matrix A, int which, uint32_t alpha, cons
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
     if (which != FFSPMV_OP_APPLY && which != FFSPMV_OP_TRANSPOSE)
         return fail(FFSPMV_ERR_INVALID_ARG, "op must be FFSPMV_OP_APPLY or FFSPMV_OP_TRANSPOSE");
-    if (!A->has_op[which]) return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built");
-    const DevOp &op = A->op[which];
+    if (!A->has_op[which] && !A->has_pan[which])
+        return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built");
+    struct { uint64_t rows, cols; } op{A->has_pan[which] ? A->pan[which].rows : A->op[which].rows,
+                                       A->has_pan[which] ? A->pan[which].cols : A->op[which].cols};
     if ((op.cols && !x_host) || (op.rows && !y_host))
         return fail(FFSPMV_ERR_INVALID_ARG, "NULL host vector");
     std::lock_guard<std::mutex> lk(A->mu);

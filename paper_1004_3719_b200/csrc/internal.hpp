@@ -116,7 +116,62 @@ struct BuildOptions {
     uint32_t long_row = 512;
     uint32_t split_chunk = 1u << 14;
     int force_acc_bits = 0;
+    int strategy = 0;          // 0 auto, 1 rows (x gathered from L2), 2 panels (x in smem)
+    uint32_t panel_rows = 0;   // 0 = default R (testing: smaller tiles)
+    uint32_t panel_cols = 0;   // 0 = default W (testing: smaller panels)
 };
+
+// ------------------------------------------------------------------ panels --
+// 2-D tiled operator for k = 1 (apply / transpose): the columns are cut into
+// panels of W columns whose slice of x is staged in shared memory (the paper's
+// column-wise split of A, with x staged on chip); the rows into
+// bands of R rows whose accumulators live in shared memory.  Tile t = p*B + b
+// holds the entries of panel p x band b sorted by (row, col), each packed in
+// one u32:  col - p*W (bits 0..15) | sign (bit 16) | row - b*R (bits 17..30).
+// A tile writes one residue per band row into partial[p][row]; a reduction
+// pass sums the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
+// spmv(y, Ai, x); reduce(y, m)").
+struct Canon;
+constexpr uint32_t PANEL_COL_BITS = 16;
+constexpr uint32_t PANEL_SIGN = 1u << 16;
+constexpr uint32_t PANEL_ROW_SHIFT = 17;
+
+struct PanelGeom {
+    uint32_t W = 0, R = 0, P = 0, B = 0;
+    uint32_t xbytes = 4;       // bytes per staged x / partial element (1, 2, 4)
+    uint32_t split = 0;        // 1: accumulate residues as two u32 halves (m > 65536)
+    uint32_t nctas = 0;        // persistent CTAs (one per SM)
+};
+
+struct HostPanel {
+    uint32_t rows = 0, cols = 0;
+    PanelGeom g;
+    std::vector<uint32_t> tp, tv;      // tile offsets, P*B + 1 each
+    std::vector<uint32_t> pent, vent;  // packed entries
+    std::vector<uint8_t> vval;         // values of vent (vbytes each)
+    std::vector<uint32_t> cta_t0;      // nctas + 1 tile boundaries
+    uint64_t nnz_pm = 0, nnz_val = 0, stream_bytes = 0;
+};
+
+struct DevPanel {
+    uint32_t rows, cols;
+    PanelGeom g;
+    const uint32_t *tp, *tv, *pent, *vent, *cta_t0;
+    const void *vval;
+    void *partial;                     // P * rows * xbytes scratch
+};
+
+// Chooses W, R, element widths for modulus m.
+PanelGeom panel_geometry(uint64_t rows, uint64_t cols, uint32_t m, const BuildOptions &bo,
+                         uint32_t nsm);
+void pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &bo, uint32_t nsm);
+uint64_t reconstruct_panels(const HostPanel &hp, uint32_t m, uint32_t vbytes, uint32_t *rr,
+                            uint32_t *rc, uint32_t *rv, uint64_t cap);
+// Column-locality of the rows layout: distinct 128 B x lines touched per
+// 256-row band divided by nonzeros (1 = no reuse, random columns).
+double gather_locality(const Canon &a);
+int launch_panel_apply(const DevPanel &op, const DevMod &M, uint32_t alpha, const uint32_t *x,
+                       uint32_t beta, uint32_t *y, void *stream);
 
 // Canonical CSR: rows sorted by column, duplicates summed mod m, zeros dropped.
 struct Canon {

@@ -35,6 +35,10 @@ def test_exports_every_declared_symbol(lib):
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(lib.EXPORTS) == declared
+    info = lib.ffspmv_analyze(1, 1, np.zeros(1, np.uint32), np.zeros(1, np.uint32),
+                              np.ones(1, np.int64), 7)
+    import ctypes
+    assert info["struct_size"] == ctypes.sizeof(lib.ffspmv_info)
     assert lib.ffspmv_version() >= 100
     assert lib.ffspmv_status_string(lib.ERR_NONSQUARE) == "FFSPMV_ERR_NONSQUARE"
 
@@ -62,6 +66,8 @@ OPTION_SETS = [
     dict(segregate_pm1=-1), dict(segregate_pm1=1, force_format=3),
     dict(band_rows=32, long_row=4), dict(band_rows=64, long_row=8, force_format=2),
     dict(force_acc_bits=96), dict(force_acc_bits=64, force_format=3),
+    dict(strategy=2), dict(strategy=2, panel_rows=32, panel_cols=32),
+    dict(strategy=2, panel_rows=64, panel_cols=96, segregate_pm1=-1),
 ]
 
 
@@ -130,6 +136,21 @@ def test_chooser_and_regimes(lib):
     for fmt, key in ((1, "bands_sell"), (2, "bands_csr"), (3, "bands_coos")):
         info = lib.ffspmv_analyze(n, n, ri, ci, val, m, force_format=fmt, band_rows=1024)
         assert info[key] == info["bands"] == 4
+
+
+def test_panel_strategy_choice(lib):
+    import synth as sy
+    M = sy.config_matrix("c2", scale=1 / 2)        # random columns, 524k x 524k
+    info = lib.ffspmv_analyze(M["rows"], M["cols"], M["row"], M["col"], M["val"], M["m"])
+    assert info["gather_locality"] > 0.7
+    assert info["strategy_apply"] == lib.STRATEGY_PANELS == info["strategy_transpose"]
+    assert info["panels"] == 8 and info["panel_bands"] == 32
+    # banded matrix: columns local -> rows layout
+    n = 1 << 19
+    ri = np.repeat(np.arange(n, dtype=np.uint32), 4)
+    ci = (ri.astype(np.int64) + np.tile(np.arange(4), n)) % n
+    info = lib.ffspmv_analyze(n, n, ri, ci.astype(np.uint32), np.full(4 * n, 3, np.int64), 65521)
+    assert info["gather_locality"] < 0.2 and info["strategy_apply"] == lib.STRATEGY_ROWS
 
 
 def test_algorithmic_bytes(lib):

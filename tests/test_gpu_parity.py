@@ -18,7 +18,9 @@ MODS = [2, 3, 27, 251, 256, 257, 65521, 65536, 65537, (1 << 20) + 7, (1 << 31) -
         (1 << 32) - 5, (1 << 32) - 1]
 OPTS = [dict(), dict(force_format=1), dict(force_format=2), dict(force_format=3),
         dict(segregate_pm1=-1), dict(band_rows=32, long_row=6), dict(force_acc_bits=96),
-        dict(force_acc_bits=64, force_format=2, long_row=3)]
+        dict(force_acc_bits=64, force_format=2, long_row=3),
+        dict(strategy=2), dict(strategy=2, panel_rows=32, panel_cols=64),
+        dict(strategy=2, panel_rows=96, panel_cols=32, segregate_pm1=-1)]
 
 
 def dev(a):
