@@ -1,6 +1,21 @@
-// Block apply Y <- alpha A X + beta Y as header templates:
-// instantiated for u32 blocks in block.cu and for the narrow sequence
-// iterate in seq.cu.
+// Block apply Y <- alpha A X + beta Y as header templates,
+// shared by ffspmv_apply_block (block.cu, u32 blocks) and the block Wiedemann
+// sequence (seq.cu, narrow iterate + fused projection).
+//
+// Lanes own vector columns: KP = min(32, pow2ceil(k)) lanes share a matrix row
+// and each owns one column, G = 32/KP rows are in flight per warp, so every
+// nonzero is read once and reused for KP columns ("we traverse the matrix only
+// once and x and y are read/written contiguously").  k > 32 loops
+// over column chunks of 32.
+//
+// SELL slices are walked slot-major: the warp loads slot j of all 32 rows with
+// one coalesced load, then each lane takes the (col, value) of each of its NR
+// rows by __shfl_sync and issues NR independent gathers of X -- NR loads in
+// flight per lane instead of a dependent walk per row.
+//
+// Results leave through an output policy `Out`:
+//   out.put(row, col, colok, residue)   called exactly once per (row, col)
+// (BlockOut: alpha/beta epilogue into Y; the sequence adds the projection).
 #pragma once
 
 #include "device.cuh"
@@ -8,7 +23,7 @@
 namespace ffspmv {
 
 void count_launch();
-constexpr int BWARPS = 4;  // warps per CTA of the block kernels
+constexpr int BWARPS = 4;  // warps per CTA of the non-persistent block kernel
 
 __device__ __forceinline__ SliceHdr load_hdr_b(const SliceHdr *p) {
     uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
@@ -21,47 +36,97 @@ static inline uint32_t total_items_b(const DevOp &op) {
     return op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
 }
 
-// =========================================================== block ========
-// Lanes own vector columns (KP lanes per row, 32/KP rows per warp pass): each
-// nonzero is broadcast to the KP lanes of its row and reused for KP columns
-// ("we traverse the matrix only once and x and y are read/written
-// contiguously").  k > 32 loops over column chunks of 32.
+template <class TY>
+struct BlockOut {
+    TY *Y;
+    uint64_t ldy;
+    uint32_t alpha, beta;
+    __device__ __forceinline__ void put(uint32_t row, uint32_t col, bool colok, uint32_t r,
+                                        const DevMod &M) {
+        if (!colok) return;
+        TY *p = Y + (uint64_t)row * ldy + col;
+        *p = (TY)epilogue(r, alpha, beta, beta ? (uint32_t)*p : 0u, M);
+    }
+    __device__ __forceinline__ void zero(uint32_t row, uint32_t col, const DevMod &M) {
+        TY *p = Y + (uint64_t)row * ldy + col;
+        *p = (TY)(beta ? mod64((uint64_t)beta * (uint32_t)*p, M) : 0u);
+    }
+};
 
-template <class Acc, class VT, int KP, class TX, class TY>
+// rows per pass of a slice: all 32 rows for KP <= 16, two passes of 16 for KP = 32
+template <int KP>
+struct SliceShape {
+    static constexpr int G = 32 / KP;
+    static constexpr int NR = (KP >= 32) ? 16 : KP;   // rows per lane per pass
+    static constexpr int PASSES = 32 / (G * NR);
+};
+
+template <class Acc, class VT, int KP, class TX, class Out>
 __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, uint32_t s,
                                             const SliceHdr &h, uint32_t lane, uint32_t k,
-                                            uint32_t alpha, const TX *__restrict__ X,
-                                            uint64_t ldx, uint32_t beta, TY *__restrict__ Y,
-                                            uint64_t ldy) {
-    constexpr uint32_t G = 32 / KP;
+                                            const TX *__restrict__ X, uint64_t ldx, Out &out) {
+    using S = SliceShape<KP>;
     const uint32_t g = lane / KP, cl = lane % KP;
+    const uint32_t m = M.m;
+    const uint32_t *pc = op.pcol + h.off_p + lane;
+    const uint32_t *vc = op.vcol + h.off_v + lane;
+    const VT *vv = reinterpret_cast<const VT *>(op.vval) + h.off_v + lane;
+    const uint32_t wp = h.wp, wv = h.wv;
     for (uint32_t c0 = 0; c0 < k; c0 += KP) {
         const uint32_t col = c0 + cl;
         const bool colok = col < k;
-        auto gat = [X, ldx, col, colok](uint32_t c) {
-            return colok ? ld_gather(X + (uint64_t)c * ldx + col) : 0u;
-        };
-        for (uint32_t rl = g; rl < h.nrows; rl += G) {
-            uint32_t row = op.perm[s * 32 + rl];
-            Acc acc;
-            walk<false>(acc, op.pcol, h.off_p + rl, 32u, (uint32_t)h.wp, op.vcol,
-                        reinterpret_cast<const VT *>(op.vval), h.off_v + rl, 32u, (uint32_t)h.wv,
-                        M.m, gat);
-            if (colok) {
-                TY *yp = Y + (uint64_t)row * ldy + col;
-                *yp = (TY)epilogue(acc.reduce(M), alpha, beta, beta ? *yp : 0u, M);
+        const TX *Xc = X + col;
+#pragma unroll 1
+        for (int pass = 0; pass < S::PASSES; ++pass) {
+            const uint32_t rbase = pass * S::G * S::NR + g;
+            Acc acc[S::NR];
+            // +-1 slots: addend x or m - x
+            uint32_t cw = wp ? ld_bcast(pc) : PAD_COL;
+            for (uint32_t j = 0; j < wp; ++j) {
+                const uint32_t cur = cw;
+                if (j + 1 < wp) cw = ld_bcast(pc + (j + 1) * 32);
+                uint32_t xv[S::NR], cs[S::NR];
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i) {
+                    cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
+                    xv[i] = (cs[i] != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (uint64_t)(cs[i] & COL_MASK) * ldx) : 0u;
+                }
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i) acc[i].add((cs[i] & SIGN_BIT) ? m - xv[i] : xv[i]);
+            }
+            // valued slots: addend a * x
+            uint32_t vw = wv ? ld_bcast(vc) : PAD_COL;
+            uint32_t aw = wv ? ld_bcast(vv) : 0u;
+            for (uint32_t j = 0; j < wv; ++j) {
+                const uint32_t cur = vw, cura = aw;
+                if (j + 1 < wv) { vw = ld_bcast(vc + (j + 1) * 32); aw = ld_bcast(vv + (j + 1) * 32); }
+                uint32_t xv[S::NR], as[S::NR];
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i) {
+                    const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
+                    as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i * S::G);
+                    xv[i] = (c != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (uint64_t)c * ldx) : 0u;
+                }
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i) acc[i].mad(as[i], xv[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < S::NR; ++i) {
+                const uint32_t r = rbase + i * S::G;
+                if (r < h.nrows) out.put(op.perm[s * 32 + r], col, colok, acc[i].reduce(M), M);
             }
         }
     }
 }
 
-template <class VT, int KP, class TX, class TY>
+// Long row: entries split over the G row groups, each lane a column; the
+// group residues are summed with __shfl_xor.  A split row is handled whole
+// by its first chunk (always exact in u96).
+template <class VT, int KP, class TX, class Out>
 __device__ __forceinline__ void block_long(const DevOp &op, const DevMod &M, uint32_t w,
                                            const LongItem &it, uint32_t lane, uint32_t k,
-                                           uint32_t alpha, const TX *__restrict__ X,
-                                           uint64_t ldx, uint32_t beta, TY *__restrict__ Y,
-                                           uint64_t ldy) {
-    if (it.chunk != 0) return;  // a split row is handled whole by its first chunk
+                                           const TX *__restrict__ X, uint64_t ldx, Out &out) {
+    if (it.chunk != 0) return;
     const uint32_t nch = it.nch_reg & 0x0FFFFFFFu;
     const LongItem last = op.longs[w + nch - 1];
     const uint32_t lp = last.off_p + last.len_p - it.off_p;
@@ -74,31 +139,27 @@ __device__ __forceinline__ void block_long(const DevOp &op, const DevMod &M, uin
         const uint32_t col = c0 + cl;
         const bool colok = col < k;
         auto gat = [X, ldx, col, colok](uint32_t c) {
-            return colok ? ld_gather(X + (uint64_t)c * ldx + col) : 0u;
+            return colok ? (uint32_t)ld_gather(X + (uint64_t)c * ldx + col) : 0u;
         };
-        Acc96 acc;  // any row length: always exact
+        Acc96 acc;
         walk<false>(acc, op.pcol, it.off_p + g, G, np, op.vcol,
                     reinterpret_cast<const VT *>(op.vval), it.off_v + g, G, nv, M.m, gat);
         uint32_t tot = sum_residues(acc.reduce(M), KP, 16, M);
-        if (g == 0 && colok) {
-            TY *yp = Y + (uint64_t)it.row * ldy + col;
-            *yp = (TY)epilogue(tot, alpha, beta, beta ? *yp : 0u, M);
-        }
+        if (g == 0) out.put(it.row, col, colok, tot, M);
     }
 }
 
-template <class Acc, class VT, int KP, class TX, class TY>
+template <class Acc, class VT, int KP, class TX, class Out>
 __device__ __forceinline__ void block_group(const DevOp &op, const DevMod &M, const CsrGroup &gr,
-                                            uint32_t lane, uint32_t k, uint32_t alpha,
-                                            const TX *__restrict__ X, uint64_t ldx,
-                                            uint32_t beta, TY *__restrict__ Y, uint64_t ldy) {
+                                            uint32_t lane, uint32_t k, const TX *__restrict__ X,
+                                            uint64_t ldx, Out &out) {
     constexpr uint32_t G = 32 / KP;
     const uint32_t g = lane / KP, cl = lane % KP;
     for (uint32_t c0 = 0; c0 < k; c0 += KP) {
         const uint32_t col = c0 + cl;
         const bool colok = col < k;
         auto gat = [X, ldx, col, colok](uint32_t c) {
-            return colok ? ld_gather(X + (uint64_t)c * ldx + col) : 0u;
+            return colok ? (uint32_t)ld_gather(X + (uint64_t)c * ldx + col) : 0u;
         };
         for (uint32_t i = g; i < gr.nrows; i += G) {
             const uint32_t li = gr.first + i;
@@ -108,49 +169,43 @@ __device__ __forceinline__ void block_group(const DevOp &op, const DevMod &M, co
             Acc acc;
             walk<false>(acc, op.pcol, p0, 1u, p1 - p0, op.vcol,
                         reinterpret_cast<const VT *>(op.vval), v0, 1u, v1 - v0, M.m, gat);
-            if (colok) {
-                TY *yp = Y + (uint64_t)row * ldy + col;
-                *yp = (TY)epilogue(acc.reduce(M), alpha, beta, beta ? *yp : 0u, M);
-            }
+            out.put(row, col, colok, acc.reduce(M), M);
         }
     }
 }
 
-template <int KP, class TY>
+// Rows with no entries (COO_S bands): the output is beta*Y (or 0), i.e. the
+// residue 0 through the policy.
+template <int KP, class Out>
 __device__ __forceinline__ void block_zero(const DevOp &op, const DevMod &M, uint32_t w,
-                                           uint32_t lane, uint32_t k, uint32_t beta,
-                                           TY *__restrict__ Y, uint64_t ldy) {
+                                           uint32_t lane, uint32_t k, Out &out) {
     constexpr uint32_t G = 32 / KP;
     const uint32_t g = lane / KP, cl = lane % KP;
     for (uint32_t i = g; i < 32; i += G) {
         uint32_t zi = w * 32 + i;
         if (zi >= op.n_zero_rows) break;
         uint32_t row = op.zero_rows[zi];
-        for (uint32_t col = cl; col < k; col += KP) {
-            TY *yp = Y + (uint64_t)row * ldy + col;
-            *yp = (TY)(beta ? mod64((uint64_t)beta * *yp, M) : 0u);
-        }
+        for (uint32_t c0 = 0; c0 < k; c0 += KP) out.put(row, c0 + cl, c0 + cl < k, 0u, M);
     }
 }
 
-template <class VT, int KP, class TX, class TY>
-__global__ void __launch_bounds__(BWARPS * 32)
-k_block(DevOp op, DevMod M, uint32_t k, uint32_t alpha, const TX *__restrict__ X,
-        uint64_t ldx, uint32_t beta, TY *__restrict__ Y, uint64_t ldy) {
-    uint32_t w = blockIdx.x * BWARPS + (threadIdx.x >> 5);
-    const uint32_t lane = threadIdx.x & 31;
+// One work item (any kind) of the block product.
+template <class VT, int KP, class TX, class Out>
+__device__ __forceinline__ void block_item(const DevOp &op, const DevMod &M, uint32_t w,
+                                           uint32_t lane, uint32_t k, const TX *__restrict__ X,
+                                           uint64_t ldx, Out &out) {
     if (w < op.n_long) {
         const LongItem it = op.longs[w];
-        block_long<VT, KP, TX, TY>(op, M, w, it, lane, k, alpha, X, ldx, beta, Y, ldy);
+        block_long<VT, KP>(op, M, w, it, lane, k, X, ldx, out);
         return;
     }
     w -= op.n_long;
     if (w < op.n_slices) {
         const SliceHdr h = load_hdr_b(op.slices + w);
         switch (h.regime) {
-            case ACC32: block_slice<Acc32, VT, KP, TX, TY>(op, M, w, h, lane, k, alpha, X, ldx, beta, Y, ldy); break;
-            case ACC64: block_slice<Acc64, VT, KP, TX, TY>(op, M, w, h, lane, k, alpha, X, ldx, beta, Y, ldy); break;
-            default: block_slice<Acc96, VT, KP, TX, TY>(op, M, w, h, lane, k, alpha, X, ldx, beta, Y, ldy); break;
+            case ACC32: block_slice<Acc32, VT, KP>(op, M, w, h, lane, k, X, ldx, out); break;
+            case ACC64: block_slice<Acc64, VT, KP>(op, M, w, h, lane, k, X, ldx, out); break;
+            default: block_slice<Acc96, VT, KP>(op, M, w, h, lane, k, X, ldx, out); break;
         }
         return;
     }
@@ -158,26 +213,33 @@ k_block(DevOp op, DevMod M, uint32_t k, uint32_t alpha, const TX *__restrict__ X
     if (w < op.n_groups) {
         const CsrGroup gr = op.groups[w];
         switch (gr.regime) {
-            case ACC32: block_group<Acc32, VT, KP, TX, TY>(op, M, gr, lane, k, alpha, X, ldx, beta, Y, ldy); break;
-            case ACC64: block_group<Acc64, VT, KP, TX, TY>(op, M, gr, lane, k, alpha, X, ldx, beta, Y, ldy); break;
-            default: block_group<Acc96, VT, KP, TX, TY>(op, M, gr, lane, k, alpha, X, ldx, beta, Y, ldy); break;
+            case ACC32: block_group<Acc32, VT, KP>(op, M, gr, lane, k, X, ldx, out); break;
+            case ACC64: block_group<Acc64, VT, KP>(op, M, gr, lane, k, X, ldx, out); break;
+            default: block_group<Acc96, VT, KP>(op, M, gr, lane, k, X, ldx, out); break;
         }
         return;
     }
     w -= op.n_groups;
-    block_zero<KP, TY>(op, M, w, lane, k, beta, Y, ldy);
+    block_zero<KP>(op, M, w, lane, k, out);
+}
+
+template <class VT, int KP, class TX, class TY>
+__global__ void __launch_bounds__(BWARPS * 32)
+k_block(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint64_t ldx, BlockOut<TY> out) {
+    const uint32_t w = blockIdx.x * BWARPS + (threadIdx.x >> 5);
+    block_item<VT, KP>(op, M, w, threadIdx.x & 31, k, X, ldx, out);
 }
 
 template <class VT, class TX, class TY>
 static void launch_block_vt(dim3 grid, dim3 block, cudaStream_t st, const DevOp &op,
-                            const DevMod &M, uint32_t k, uint32_t alpha, const TX *X,
-                            uint64_t ldx, uint32_t beta, TY *Y, uint64_t ldy) {
-    if (k <= 1) k_block<VT, 1, TX, TY><<<grid, block, 0, st>>>(op, M, k, alpha, X, ldx, beta, Y, ldy);
-    else if (k <= 2) k_block<VT, 2, TX, TY><<<grid, block, 0, st>>>(op, M, k, alpha, X, ldx, beta, Y, ldy);
-    else if (k <= 4) k_block<VT, 4, TX, TY><<<grid, block, 0, st>>>(op, M, k, alpha, X, ldx, beta, Y, ldy);
-    else if (k <= 8) k_block<VT, 8, TX, TY><<<grid, block, 0, st>>>(op, M, k, alpha, X, ldx, beta, Y, ldy);
-    else if (k <= 16) k_block<VT, 16, TX, TY><<<grid, block, 0, st>>>(op, M, k, alpha, X, ldx, beta, Y, ldy);
-    else k_block<VT, 32, TX, TY><<<grid, block, 0, st>>>(op, M, k, alpha, X, ldx, beta, Y, ldy);
+                            const DevMod &M, uint32_t k, const TX *X, uint64_t ldx,
+                            BlockOut<TY> out) {
+    if (k <= 1) k_block<VT, 1, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+    else if (k <= 2) k_block<VT, 2, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+    else if (k <= 4) k_block<VT, 4, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+    else if (k <= 8) k_block<VT, 8, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+    else if (k <= 16) k_block<VT, 16, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+    else k_block<VT, 32, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
 }
 
 template <class TX, class TY>
@@ -187,14 +249,14 @@ int launch_block_t(const DevOp &op, const DevMod &M, uint32_t k, uint32_t alpha,
     if (items == 0) return 0;
     dim3 grid((items + BWARPS - 1) / BWARPS), block(BWARPS * 32);
     cudaStream_t st = (cudaStream_t)stream;
+    BlockOut<TY> out{Y, ldy, alpha, beta};
     switch (M.vbytes) {
-        case 1: launch_block_vt<uint8_t, TX, TY>(grid, block, st, op, M, k, alpha, X, ldx, beta, Y, ldy); break;
-        case 2: launch_block_vt<uint16_t, TX, TY>(grid, block, st, op, M, k, alpha, X, ldx, beta, Y, ldy); break;
-        default: launch_block_vt<uint32_t, TX, TY>(grid, block, st, op, M, k, alpha, X, ldx, beta, Y, ldy); break;
+        case 1: launch_block_vt<uint8_t, TX, TY>(grid, block, st, op, M, k, X, ldx, out); break;
+        case 2: launch_block_vt<uint16_t, TX, TY>(grid, block, st, op, M, k, X, ldx, out); break;
+        default: launch_block_vt<uint32_t, TX, TY>(grid, block, st, op, M, k, X, ldx, out); break;
     }
     count_launch();
     return (int)cudaGetLastError();
 }
-
 
 }  // namespace ffspmv

@@ -23,6 +23,8 @@ void count_launch();
 namespace {
 
 constexpr int PANEL_THREADS = 1024;
+constexpr int PB = 8;                       // entries per stream per thread per round
+constexpr uint32_t PANEL_NONE = 0xFFFFFFFFu;  // no entry (bit 31 is never set in a packed word)
 
 template <class IT>
 __device__ __forceinline__ void st_partial(IT *p, uint32_t v) {
@@ -67,49 +69,35 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
             cur_p = p;
         }
         __syncthreads();
-        // +-1 entries: addend x or m - x, both < m (0 stays 0)
+        // One round issues every load of up to PB +-1 and PB valued entries per
+        // thread before the first shared-memory op, so a tile costs about one
+        // memory round trip (+-1 addend: x or m - x; valued: (a*x) mod m).
         {
-            const uint32_t e0 = op.tp[t], e1 = op.tp[t + 1];
-            uint32_t e = e0 + threadIdx.x;
-            for (; e + 3 * PANEL_THREADS < e1; e += 4 * PANEL_THREADS) {
-                uint32_t w[4];
+            const uint32_t p0 = op.tp[t], np = op.tp[t + 1] - p0;
+            const uint32_t v0 = op.tv[t], nv = op.tv[t + 1] - v0;
+            const uint32_t nmax = max(np, nv);
+            for (uint32_t base = threadIdx.x; base < nmax; base += PB * PANEL_THREADS) {
+                uint32_t w[PB], vw[PB], va[PB];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) w[u] = ld_stream(op.pent + e + u * PANEL_THREADS);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint32_t xv = sx[w[u] & 0xFFFFu];
-                    uint32_t a = (w[u] & PANEL_SIGN) ? (xv ? m - xv : 0u) : xv;
-                    acc_add<SPLIT>(acc, g.R, w[u] >> PANEL_ROW_SHIFT, a);
-                }
-            }
-            for (; e < e1; e += PANEL_THREADS) {
-                uint32_t w = ld_stream(op.pent + e);
-                uint32_t xv = sx[w & 0xFFFFu];
-                uint32_t a = (w & PANEL_SIGN) ? (xv ? m - xv : 0u) : xv;
-                acc_add<SPLIT>(acc, g.R, w >> PANEL_ROW_SHIFT, a);
-            }
-        }
-        // valued entries: addend (a * x) mod m
-        {
-            const uint32_t e0 = op.tv[t], e1 = op.tv[t + 1];
-            uint32_t e = e0 + threadIdx.x;
-            for (; e + 3 * PANEL_THREADS < e1; e += 4 * PANEL_THREADS) {
-                uint32_t w[4], a[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    w[u] = ld_stream(op.vent + e + u * PANEL_THREADS);
-                    a[u] = ld_stream(vval + e + u * PANEL_THREADS);
+                for (int u = 0; u < PB; ++u) {
+                    const uint32_t e = base + u * PANEL_THREADS;
+                    w[u] = e < np ? ld_stream(op.pent + p0 + e) : PANEL_NONE;
+                    vw[u] = e < nv ? ld_stream(op.vent + v0 + e) : PANEL_NONE;
+                    va[u] = e < nv ? ld_stream(vval + v0 + e) : 0u;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint32_t xv = sx[w[u] & 0xFFFFu];
-                    acc_add<SPLIT>(acc, g.R, w[u] >> PANEL_ROW_SHIFT, mod64((uint64_t)a[u] * xv, M));
+                for (int u = 0; u < PB; ++u) {
+                    if (w[u] != PANEL_NONE) {
+                        const uint32_t xv = sx[w[u] & 0xFFFFu];
+                        const uint32_t a = (w[u] & PANEL_SIGN) ? (xv ? m - xv : 0u) : xv;
+                        acc_add<SPLIT>(acc, g.R, w[u] >> PANEL_ROW_SHIFT, a);
+                    }
+                    if (vw[u] != PANEL_NONE) {
+                        const uint32_t xv = sx[vw[u] & 0xFFFFu];
+                        acc_add<SPLIT>(acc, g.R, vw[u] >> PANEL_ROW_SHIFT,
+                                       mod64((uint64_t)va[u] * xv, M));
+                    }
                 }
-            }
-            for (; e < e1; e += PANEL_THREADS) {
-                uint32_t w = ld_stream(op.vent + e), a = ld_stream(vval + e);
-                uint32_t xv = sx[w & 0xFFFFu];
-                acc_add<SPLIT>(acc, g.R, w >> PANEL_ROW_SHIFT, mod64((uint64_t)a * xv, M));
             }
         }
         __syncthreads();

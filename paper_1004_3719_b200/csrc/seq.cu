@@ -60,7 +60,7 @@ __global__ void k_seq_widen(const IT *__restrict__ V, uint64_t n, uint32_t *__re
 template <class IT, class Acc>
 __global__ void __launch_bounds__(PROJ_THREADS)
 k_project(const IT *__restrict__ V, const IT *__restrict__ Uc, uint64_t n, uint32_t k,
-          uint32_t ku, uint32_t tr, DevMod M, uint32_t *__restrict__ partial) {
+          uint32_t ku, uint32_t ldu, uint32_t tr, DevMod M, uint32_t *__restrict__ partial) {
     extern __shared__ uint32_t sm[];
     uint32_t *su = sm;               // tr x ku
     uint32_t *sv = sm + tr * ku;     // tr x k
@@ -79,7 +79,8 @@ k_project(const IT *__restrict__ V, const IT *__restrict__ Uc, uint64_t n, uint3
         for (uint64_t rb = r0; rb < r1; rb += tr) {
             const uint32_t nr = (uint32_t)((r1 - rb < tr) ? r1 - rb : tr);
             __syncthreads();
-            for (uint32_t i = threadIdx.x; i < nr * ku; i += PROJ_THREADS) su[i] = Uc[rb * ku + i];
+            for (uint32_t i = threadIdx.x; i < nr * ku; i += PROJ_THREADS)
+                su[i] = Uc[(rb + i / ku) * ldu + i % ku];
             for (uint32_t i = threadIdx.x; i < nr * k; i += PROJ_THREADS) sv[i] = V[rb * k + i];
             __syncthreads();
             for (uint32_t r = 0; r < nr; ++r) {
@@ -107,32 +108,135 @@ __global__ void k_seq_finalize(const uint32_t *__restrict__ partial, uint32_t nc
     if (lane == 0) S[p] = mod64(s, M);
 }
 
+// ------------------------------------------------------------- fused step ---
+// V_{t+1} = A V_t with the projection U^T V_{t+1} fused into the SpMM
+// epilogue (SURVEY §8 a-8 + a-9): each lane owns one column of the iterate and
+// accumulates P[a] += U[row][a] * V_{t+1}[row][col] for the rows it computes,
+// exactly (u64 when every partial sum < 2^64, else u96).  U is staged in a
+// padded internal copy (KUP columns, 16-byte rows) so its rows load as uint4.
+// Persistent grid; the warps also finalise the previous step's S from its
+// CTA partials, so one launch per step.
+constexpr int SEQ_WARPS = 8;
+
+template <class IT, int KUP, class PAcc>
+struct SeqOut {
+    IT *V;
+    const IT *U;
+    uint32_t k;
+    PAcc P[KUP];
+    __device__ __forceinline__ void put(uint32_t row, uint32_t col, bool colok, uint32_t r,
+                                        const DevMod &M) {
+        if (!colok) return;
+        V[(uint64_t)row * k + col] = (IT)r;
+        constexpr int PER = 16 / sizeof(IT);
+        const uint4 *u4 = reinterpret_cast<const uint4 *>(U + (uint64_t)row * KUP);
+#pragma unroll
+        for (int q = 0; q < KUP / PER; ++q) {
+            const uint4 w = __ldg(u4 + q);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                uint32_t ua;
+                if constexpr (sizeof(IT) == 2) ua = (ws[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                else ua = ws[e];
+                P[q * PER + e].mad(ua, r);
+            }
+        }
+    }
+};
+
+__device__ __forceinline__ void finalize_pairs(const uint32_t *__restrict__ part, uint32_t nctas,
+                                               uint32_t pairs, uint32_t gw, uint32_t nw,
+                                               uint32_t lane, const DevMod &M,
+                                               uint32_t *__restrict__ S) {
+    for (uint32_t p = gw; p < pairs; p += nw) {
+        uint64_t s = 0;
+        for (uint32_t c = lane; c < nctas; c += 32) s += part[(uint64_t)c * pairs + p];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        if (lane == 0) S[p] = mod64(s, M);
+    }
+}
+
+template <class VT, int KP, class IT, int KUP, class PAcc>
+__global__ void __launch_bounds__(SEQ_WARPS * 32)
+k_seq_step(DevOp op, DevMod M, uint32_t k, uint32_t ku, const IT *__restrict__ Vin,
+           IT *__restrict__ Vout, const IT *__restrict__ Uc, uint32_t *__restrict__ part_out,
+           const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev) {
+    __shared__ uint32_t red[SEQ_WARPS][KUP][KP];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * SEQ_WARPS + warp, nw = gridDim.x * SEQ_WARPS;
+    const uint32_t pairs = ku * k;
+    if (part_prev) finalize_pairs(part_prev, nprev, pairs, gw, nw, lane, M, S_prev);
+    SeqOut<IT, KUP, PAcc> out{Vout, Uc, k};
+    const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    for (uint32_t w = gw; w < items; w += nw) block_item<VT, KP>(op, M, w, lane, k, Vin, k, out);
+    // lanes g*KP + cl hold partials of column cl: sum the groups, then the warps
+#pragma unroll
+    for (int a = 0; a < KUP; ++a) {
+        uint32_t r = sum_residues(out.P[a].reduce(M), KP, 16, M);
+        if (lane < KP) red[warp][a][lane] = r;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < pairs; i += SEQ_WARPS * 32) {
+        const uint32_t a = i / k, c = i - a * k;
+        uint64_t s = 0;
+#pragma unroll
+        for (int w = 0; w < SEQ_WARPS; ++w) s += red[w][a][c];
+        part_out[(uint64_t)blockIdx.x * pairs + i] = mod64(s, M);
+    }
+}
+
+template <class IT, int KUP>
+__global__ void k_seq_prep_pad(const uint32_t *__restrict__ X, const uint32_t *__restrict__ U,
+                               uint64_t n, uint32_t k, uint32_t ku, IT *__restrict__ V0,
+                               IT *__restrict__ Uc) {
+    const uint64_t nk = n * k, nu = n * KUP;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nk + nu;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i < nk) {
+            V0[i] = (IT)X[i];
+        } else {
+            const uint64_t j = i - nk, r = j / KUP;
+            const uint32_t a = (uint32_t)(j - r * KUP);
+            Uc[j] = a < ku ? (IT)U[r * ku + a] : (IT)0;
+        }
+    }
+}
+
 template <class IT>
 struct SeqLayout {
     IT *V[2];
-    IT *Uc;
-    uint32_t *partial;
+    IT *Uc;          // n x ku (unfused path) or n x KUP padded (fused path)
+    uint32_t *partial[2];
     size_t bytes;
 };
+
+inline uint32_t kup_for(uint32_t ku) { return ku <= 8 ? 8 : ku <= 16 ? 16 : 32; }
+inline bool fused_ok(uint32_t k, uint32_t ku) { return k <= 32 && ku <= 32; }
+constexpr uint32_t MAX_STEP_CTAS_PER_SM = 8;
 
 template <class IT>
 SeqLayout<IT> layout(void *ws, uint64_t n, uint32_t k, uint32_t ku, uint32_t nctas) {
     SeqLayout<IT> L{};
     char *p = (char *)ws;
     size_t off = 0;
+    const uint32_t ucols = fused_ok(k, ku) ? kup_for(ku) : ku;
+    const uint32_t maxc = std::max<uint32_t>(nctas, (uint32_t)num_sms() * MAX_STEP_CTAS_PER_SM);
     size_t vb = align256(n * (size_t)k * sizeof(IT));
-    size_t ub = align256(n * (size_t)ku * sizeof(IT));
-    size_t pb = align256((size_t)nctas * ku * k * sizeof(uint32_t));
+    size_t ub = align256(n * (size_t)ucols * sizeof(IT));
+    size_t pb = align256((size_t)maxc * ku * k * sizeof(uint32_t));
     L.V[0] = (IT *)(p + off); off += vb;
     L.V[1] = (IT *)(p + off); off += vb;
     L.Uc = (IT *)(p + off); off += ub;
-    L.partial = (uint32_t *)(p + off); off += pb;
+    L.partial[0] = (uint32_t *)(p + off); off += pb;
+    L.partial[1] = (uint32_t *)(p + off); off += pb;
     L.bytes = off;
     return L;
 }
 
+// Projection partials of V (k_project) + optional finalisation into S_t.
 template <class IT>
-int project(const DevOp &op, const DevMod &M, const IT *V, const IT *Uc, uint64_t n, uint32_t k,
+int project(const IT *V, const IT *Uc, uint32_t ldu, const DevMod &M, uint64_t n, uint32_t k,
             uint32_t ku, uint32_t *partial, uint32_t nctas, uint32_t *S_t, cudaStream_t st) {
     uint32_t tr = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(64, 12288 / (k + ku)));
     size_t smem = (size_t)tr * (k + ku) * sizeof(uint32_t);
@@ -140,15 +244,68 @@ int project(const DevOp &op, const DevMod &M, const IT *V, const IT *Uc, uint64_
     typedef unsigned __int128 u128;
     bool wide = (u128)per * (u128)(M.m - 1) * (u128)(M.m - 1) > (u128)~(uint64_t)0;
     if (wide)
-        k_project<IT, Acc96><<<nctas, PROJ_THREADS, smem, st>>>(V, Uc, n, k, ku, tr, M, partial);
+        k_project<IT, Acc96><<<nctas, PROJ_THREADS, smem, st>>>(V, Uc, n, k, ku, ldu, tr, M, partial);
     else
-        k_project<IT, Acc64><<<nctas, PROJ_THREADS, smem, st>>>(V, Uc, n, k, ku, tr, M, partial);
+        k_project<IT, Acc64><<<nctas, PROJ_THREADS, smem, st>>>(V, Uc, n, k, ku, ldu, tr, M, partial);
     count_launch();
-    uint32_t pairs = ku * k;
-    k_seq_finalize<<<(pairs + 7) / 8, 256, 0, st>>>(partial, nctas, pairs, M, S_t);
-    count_launch();
-    (void)op;
+    if (S_t) {
+        uint32_t pairs = ku * k;
+        k_seq_finalize<<<(pairs + 7) / 8, 256, 0, st>>>(partial, nctas, pairs, M, S_t);
+        count_launch();
+    }
     return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------- fused launch ---
+template <class VT, int KP, class IT, int KUP, class PAcc>
+int launch_step_t(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku, const IT *Vin,
+                  IT *Vout, const IT *Uc, uint32_t *part_out, const uint32_t *part_prev,
+                  uint32_t nprev, uint32_t *S_prev, uint32_t &nctas_out, cudaStream_t st) {
+    auto kern = k_seq_step<VT, KP, IT, KUP, PAcc>;
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SEQ_WARPS * 32, 0);
+        occ = std::max(1, std::min<int>(occ, (int)MAX_STEP_CTAS_PER_SM));
+    }
+    uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    uint32_t nctas = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)num_sms() * occ, (items + SEQ_WARPS - 1) / SEQ_WARPS));
+    kern<<<nctas, SEQ_WARPS * 32, 0, st>>>(op, M, k, ku, Vin, Vout, Uc, part_out, part_prev, nprev,
+                                          S_prev);
+    count_launch();
+    nctas_out = nctas;
+    return (int)cudaGetLastError();
+}
+
+template <class VT, class IT, int KUP, class PAcc>
+int launch_step_kp(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku, const IT *Vin,
+                   IT *Vout, const IT *Uc, uint32_t *po, const uint32_t *pp, uint32_t np,
+                   uint32_t *Sp, uint32_t &nc, cudaStream_t st) {
+    if (k <= 1) return launch_step_t<VT, 1, IT, KUP, PAcc>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    if (k <= 2) return launch_step_t<VT, 2, IT, KUP, PAcc>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    if (k <= 4) return launch_step_t<VT, 4, IT, KUP, PAcc>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    if (k <= 8) return launch_step_t<VT, 8, IT, KUP, PAcc>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    if (k <= 16) return launch_step_t<VT, 16, IT, KUP, PAcc>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    return launch_step_t<VT, 32, IT, KUP, PAcc>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+}
+
+template <class IT>
+int launch_step(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku, const IT *Vin, IT *Vout,
+                const IT *Uc, uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp,
+                uint32_t &nc, cudaStream_t st) {
+    // u16 iterate (m <= 65536): products < 2^32, any n < 2^31 rows fit u64;
+    // u32 iterate: exact in u96
+    if constexpr (sizeof(IT) == 2) {
+        if (M.vbytes == 1) {
+            if (ku <= 16) return launch_step_kp<uint8_t, IT, 16, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+            return launch_step_kp<uint8_t, IT, 32, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+        }
+        if (ku <= 16) return launch_step_kp<uint16_t, IT, 16, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+        return launch_step_kp<uint16_t, IT, 32, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    } else {
+        if (ku <= 16) return launch_step_kp<uint32_t, IT, 16, Acc96>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+        return launch_step_kp<uint32_t, IT, 32, Acc96>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    }
 }
 
 template <class IT>
@@ -163,29 +320,59 @@ int run_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X
             return (int)cudaMemcpyAsync(V_out, X, n * (size_t)k * 4, cudaMemcpyDeviceToDevice, st);
         return 0;
     }
+    const bool fused = fused_ok(k, ku);
+    const uint32_t ldu = fused ? kup_for(ku) : ku;
+    const uint32_t pairs = ku * k;
     int err;
     {
-        uint64_t tot = n * (uint64_t)(k + ku);
+        uint64_t tot = n * (uint64_t)(k + ldu);
         uint32_t blocks = (uint32_t)std::min<uint64_t>((tot + 255) / 256, (uint64_t)num_sms() * 8);
-        if (blocks) {
+        if (fused) {
+            if (ldu == 16)
+                k_seq_prep_pad<IT, 16><<<blocks, 256, 0, st>>>(X, U ? U : X, n, k, ku, W.V[0], W.Uc);
+            else
+                k_seq_prep_pad<IT, 32><<<blocks, 256, 0, st>>>(X, U ? U : X, n, k, ku, W.V[0], W.Uc);
+        } else {
             k_seq_prep<IT><<<blocks, 256, 0, st>>>(X, U ? U : X, n * (uint64_t)k, n * (uint64_t)ku,
                                                   W.V[0], W.Uc);
-            count_launch();
         }
+        count_launch();
     }
-    for (uint64_t t = 0; t < L; ++t) {
-        const IT *Vt = W.V[t & 1];
-        if ((err = project<IT>(op, M, Vt, W.Uc, n, k, ku, W.partial, nctas,
-                               S + t * (uint64_t)ku * k, st)))
-            return err;
-        if (t + 1 < L) {
-            if ((err = launch_block_t<IT, IT>(op, M, k, 1u, Vt, k, 0u, W.V[(t + 1) & 1], k,
-                                              (void *)st)))
+    if (!fused) {
+        for (uint64_t t = 0; t < L; ++t) {
+            const IT *Vt = W.V[t & 1];
+            if ((err = project<IT>(Vt, W.Uc, ldu, M, n, k, ku, W.partial[0], nctas, S + t * pairs, st)))
                 return err;
-        } else if (V_out) {
-            if ((err = launch_block_t<IT, uint32_t>(op, M, k, 1u, Vt, k, 0u, V_out, k, (void *)st)))
-                return err;
+            if (t + 1 < L) {
+                if ((err = launch_block_t<IT, IT>(op, M, k, 1u, Vt, k, 0u, W.V[(t + 1) & 1], k, (void *)st)))
+                    return err;
+            } else if (V_out) {
+                if ((err = launch_block_t<IT, uint32_t>(op, M, k, 1u, Vt, k, 0u, V_out, k, (void *)st)))
+                    return err;
+            }
         }
+        return (int)cudaGetLastError();
+    }
+    // fused: S_0 partials from the projection kernel; step t (1..L-1) computes
+    // V_t with its projection partials and finalises S_{t-1}
+    if ((err = project<IT>(W.V[0], W.Uc, ldu, M, n, k, ku, W.partial[0], nctas, nullptr, st)))
+        return err;
+    uint32_t nprev = nctas;
+    for (uint64_t t = 1; t < L; ++t) {
+        uint32_t nc = 0;
+        if ((err = launch_step<IT>(op, M, k, ku, W.V[(t - 1) & 1], W.V[t & 1], W.Uc,
+                                   W.partial[t & 1], W.partial[(t - 1) & 1], nprev,
+                                   S + (t - 1) * pairs, nc, st)))
+            return err;
+        nprev = nc;
+    }
+    k_seq_finalize<<<(pairs + 7) / 8, 256, 0, st>>>(W.partial[(L - 1) & 1], nprev, pairs, M,
+                                                   S + (L - 1) * pairs);
+    count_launch();
+    if (V_out) {
+        if ((err = launch_block_t<IT, uint32_t>(op, M, k, 1u, W.V[(L - 1) & 1], k, 0u, V_out, k,
+                                                (void *)st)))
+            return err;
     }
     return (int)cudaGetLastError();
 }
