@@ -211,7 +211,7 @@ struct SeqLayout {
     size_t bytes;
 };
 
-inline uint32_t kup_for(uint32_t ku) { return ku <= 8 ? 8 : ku <= 16 ? 16 : 32; }
+inline uint32_t kup_for(uint32_t ku) { return ku <= 16 ? 16 : 32; }
 inline bool fused_ok(uint32_t k, uint32_t ku) { return k <= 32 && ku <= 32; }
 constexpr uint32_t MAX_STEP_CTAS_PER_SM = 8;
 
