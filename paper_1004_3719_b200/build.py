@@ -65,10 +65,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     logs = []
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
-            for out in ex.map(_run, jobs):
+            for job, out in zip(jobs, ex.map(_run, jobs)):
                 logs.append(out)
-        with open(os.path.join(BUILD, "ptxas.log"), "a") as f:
-            f.write("\n".join(logs))
+                with open(job[job.index("-o") + 1] + ".log", "w") as f:   # per-object ptxas report
+                    f.write(out)
     if force or jobs or _newer(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
         _run([NVCC, "-shared", *GENCODE, "-cudart", "static", "-o", tmp, *objs,

@@ -526,6 +526,8 @@ ffspmv_status ffspmv_apply_block(ffspmv_matrix A, uint32_t k, uint32_t alpha, co
     if ((op.cols && !X) || (op.rows && !Y)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL block");
     if (overlaps(X, op.cols * ldx * 4, Y, op.rows * ldy * 4))
         return fail(FFSPMV_ERR_INVALID_ARG, "X overlaps Y");
+    if ((uint64_t)op.cols * ldx >= (1ull << 32))
+        return fail(FFSPMV_ERR_DIM, "cols * ldx must be < 2^32 elements");
     alpha %= A->m;
     beta %= A->m;
     DeviceGuard guard(A->device);

@@ -53,19 +53,20 @@ struct BlockOut {
     }
 };
 
-// rows per pass of a slice: all 32 rows for KP <= 16, two passes of 16 for KP = 32
-template <int KP>
+// G = 32/KP rows in flight per warp, NR rows per lane per pass (<= NRMAX,
+// bounding the accumulator registers), PASSES passes over the slice.
+template <int KP, int NRMAX>
 struct SliceShape {
     static constexpr int G = 32 / KP;
-    static constexpr int NR = (KP >= 32) ? 16 : KP;   // rows per lane per pass
+    static constexpr int NR = KP < NRMAX ? KP : NRMAX;
     static constexpr int PASSES = 32 / (G * NR);
 };
 
-template <class Acc, class VT, int KP, class TX, class Out>
+template <class Acc, class VT, int KP, int NRMAX, class TX, class Out>
 __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, uint32_t s,
                                             const SliceHdr &h, uint32_t lane, uint32_t k,
-                                            const TX *__restrict__ X, uint64_t ldx, Out &out) {
-    using S = SliceShape<KP>;
+                                            const TX *__restrict__ X, uint32_t ldx, Out &out) {
+    using S = SliceShape<KP, NRMAX>;
     const uint32_t g = lane / KP, cl = lane % KP;
     const uint32_t m = M.m;
     const uint32_t *pc = op.pcol + h.off_p + lane;
@@ -89,7 +90,7 @@ __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, ui
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i) {
                     cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
-                    xv[i] = (cs[i] != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (uint64_t)(cs[i] & COL_MASK) * ldx) : 0u;
+                    xv[i] = (cs[i] != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (size_t)((cs[i] & COL_MASK) * ldx)) : 0u;
                 }
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i) acc[i].add((cs[i] & SIGN_BIT) ? m - xv[i] : xv[i]);
@@ -105,7 +106,7 @@ __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, ui
                 for (int i = 0; i < S::NR; ++i) {
                     const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
                     as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i * S::G);
-                    xv[i] = (c != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (uint64_t)c * ldx) : 0u;
+                    xv[i] = (c != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (size_t)(c * ldx)) : 0u;
                 }
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i) acc[i].mad(as[i], xv[i]);
@@ -125,7 +126,7 @@ __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, ui
 template <class VT, int KP, class TX, class Out>
 __device__ __forceinline__ void block_long(const DevOp &op, const DevMod &M, uint32_t w,
                                            const LongItem &it, uint32_t lane, uint32_t k,
-                                           const TX *__restrict__ X, uint64_t ldx, Out &out) {
+                                           const TX *__restrict__ X, uint32_t ldx, Out &out) {
     if (it.chunk != 0) return;
     const uint32_t nch = it.nch_reg & 0x0FFFFFFFu;
     const LongItem last = op.longs[w + nch - 1];
@@ -139,7 +140,7 @@ __device__ __forceinline__ void block_long(const DevOp &op, const DevMod &M, uin
         const uint32_t col = c0 + cl;
         const bool colok = col < k;
         auto gat = [X, ldx, col, colok](uint32_t c) {
-            return colok ? (uint32_t)ld_gather(X + (uint64_t)c * ldx + col) : 0u;
+            return colok ? (uint32_t)ld_gather(X + (size_t)(c * ldx + col)) : 0u;
         };
         Acc96 acc;
         walk<false>(acc, op.pcol, it.off_p + g, G, np, op.vcol,
@@ -152,14 +153,14 @@ __device__ __forceinline__ void block_long(const DevOp &op, const DevMod &M, uin
 template <class Acc, class VT, int KP, class TX, class Out>
 __device__ __forceinline__ void block_group(const DevOp &op, const DevMod &M, const CsrGroup &gr,
                                             uint32_t lane, uint32_t k, const TX *__restrict__ X,
-                                            uint64_t ldx, Out &out) {
+                                            uint32_t ldx, Out &out) {
     constexpr uint32_t G = 32 / KP;
     const uint32_t g = lane / KP, cl = lane % KP;
     for (uint32_t c0 = 0; c0 < k; c0 += KP) {
         const uint32_t col = c0 + cl;
         const bool colok = col < k;
         auto gat = [X, ldx, col, colok](uint32_t c) {
-            return colok ? (uint32_t)ld_gather(X + (uint64_t)c * ldx + col) : 0u;
+            return colok ? (uint32_t)ld_gather(X + (size_t)(c * ldx + col)) : 0u;
         };
         for (uint32_t i = g; i < gr.nrows; i += G) {
             const uint32_t li = gr.first + i;
@@ -190,10 +191,10 @@ __device__ __forceinline__ void block_zero(const DevOp &op, const DevMod &M, uin
 }
 
 // One work item (any kind) of the block product.
-template <class VT, int KP, class TX, class Out>
+template <class VT, int KP, int NRMAX, class TX, class Out>
 __device__ __forceinline__ void block_item(const DevOp &op, const DevMod &M, uint32_t w,
                                            uint32_t lane, uint32_t k, const TX *__restrict__ X,
-                                           uint64_t ldx, Out &out) {
+                                           uint32_t ldx, Out &out) {
     if (w < op.n_long) {
         const LongItem it = op.longs[w];
         block_long<VT, KP>(op, M, w, it, lane, k, X, ldx, out);
@@ -203,9 +204,9 @@ __device__ __forceinline__ void block_item(const DevOp &op, const DevMod &M, uin
     if (w < op.n_slices) {
         const SliceHdr h = load_hdr_b(op.slices + w);
         switch (h.regime) {
-            case ACC32: block_slice<Acc32, VT, KP>(op, M, w, h, lane, k, X, ldx, out); break;
-            case ACC64: block_slice<Acc64, VT, KP>(op, M, w, h, lane, k, X, ldx, out); break;
-            default: block_slice<Acc96, VT, KP>(op, M, w, h, lane, k, X, ldx, out); break;
+            case ACC32: block_slice<Acc32, VT, KP, NRMAX>(op, M, w, h, lane, k, X, ldx, out); break;
+            case ACC64: block_slice<Acc64, VT, KP, NRMAX>(op, M, w, h, lane, k, X, ldx, out); break;
+            default: block_slice<Acc96, VT, KP, (NRMAX > 8 ? 8 : NRMAX)>(op, M, w, h, lane, k, X, ldx, out); break;
         }
         return;
     }
@@ -225,14 +226,14 @@ __device__ __forceinline__ void block_item(const DevOp &op, const DevMod &M, uin
 
 template <class VT, int KP, class TX, class TY>
 __global__ void __launch_bounds__(BWARPS * 32)
-k_block(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint64_t ldx, BlockOut<TY> out) {
+k_block(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint32_t ldx, BlockOut<TY> out) {
     const uint32_t w = blockIdx.x * BWARPS + (threadIdx.x >> 5);
-    block_item<VT, KP>(op, M, w, threadIdx.x & 31, k, X, ldx, out);
+    block_item<VT, KP, 16>(op, M, w, threadIdx.x & 31, k, X, ldx, out);
 }
 
 template <class VT, class TX, class TY>
 static void launch_block_vt(dim3 grid, dim3 block, cudaStream_t st, const DevOp &op,
-                            const DevMod &M, uint32_t k, const TX *X, uint64_t ldx,
+                            const DevMod &M, uint32_t k, const TX *X, uint32_t ldx,
                             BlockOut<TY> out) {
     if (k <= 1) k_block<VT, 1, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
     else if (k <= 2) k_block<VT, 2, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
@@ -250,10 +251,13 @@ int launch_block_t(const DevOp &op, const DevMod &M, uint32_t k, uint32_t alpha,
     dim3 grid((items + BWARPS - 1) / BWARPS), block(BWARPS * 32);
     cudaStream_t st = (cudaStream_t)stream;
     BlockOut<TY> out{Y, ldy, alpha, beta};
+    // X is indexed with 32-bit element offsets (one IMAD.WIDE per gather)
+    if ((uint64_t)op.cols * ldx >= (1ull << 32)) return (int)cudaErrorInvalidValue;
+    const uint32_t ld32 = (uint32_t)ldx;
     switch (M.vbytes) {
-        case 1: launch_block_vt<uint8_t, TX, TY>(grid, block, st, op, M, k, X, ldx, out); break;
-        case 2: launch_block_vt<uint16_t, TX, TY>(grid, block, st, op, M, k, X, ldx, out); break;
-        default: launch_block_vt<uint32_t, TX, TY>(grid, block, st, op, M, k, X, ldx, out); break;
+        case 1: launch_block_vt<uint8_t, TX, TY>(grid, block, st, op, M, k, X, ld32, out); break;
+        case 2: launch_block_vt<uint16_t, TX, TY>(grid, block, st, op, M, k, X, ld32, out); break;
+        default: launch_block_vt<uint32_t, TX, TY>(grid, block, st, op, M, k, X, ld32, out); break;
     }
     count_launch();
     return (int)cudaGetLastError();

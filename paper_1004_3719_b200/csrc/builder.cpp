@@ -33,6 +33,8 @@ DevMod make_mod(uint32_t m) {
     u128 two64 = (u128)1 << 64;
     d.mu = (uint64_t)(two64 / m);
     d.r64 = (uint64_t)(two64 % m);
+    d.mu32 = (uint32_t)std::min<uint64_t>((1ull << 32) / m, 0xFFFFFFFFull);
+    d.pad_ = 0;
     return d;
 }
 

@@ -64,6 +64,12 @@ __device__ __forceinline__ uint32_t mod64(uint64_t x, const DevMod &M) {
     uint64_t r = x - q * (uint64_t)M.m;
     return (uint32_t)(r >= M.m ? r - M.m : r);
 }
+// 32-bit Barrett for x < 2^32 and m <= 2^16 (mu32 = floor(2^32/m)): the same
+// one-correction argument; r < 2m <= 2^17 cannot overflow.
+__device__ __forceinline__ uint32_t mod32(uint32_t x, const DevMod &M) {
+    uint32_t r = x - __umulhi(x, M.mu32) * M.m;
+    return r >= M.m ? r - M.m : r;
+}
 // (hi * 2^64 + lo) mod m, hi < 2^32: hi mod m < m, (hi mod m)*(2^64 mod m) +
 // (lo mod m) < m^2 + m < 2^64.
 __device__ __forceinline__ uint32_t mod96(uint32_t hi, uint64_t lo, const DevMod &M) {
@@ -88,20 +94,20 @@ struct Acc64 {
     __device__ __forceinline__ void mad(uint32_t a, uint32_t x) { s += (uint64_t)a * x; }
     __device__ __forceinline__ uint32_t reduce(const DevMod &M) const { return mod64(s, M); }
 };
+// u96 = lo (u64 register pair) + h * 2^64: a MAD lowers to one
+// IMAD.WIDE.U32 with carry-out plus an IADD3.X that can merge two carries.
 struct Acc96 {
-    uint32_t l0, l1, h;
-    __device__ __forceinline__ Acc96() : l0(0), l1(0), h(0) {}
+    uint64_t lo;
+    uint32_t h;
+    __device__ __forceinline__ Acc96() : lo(0), h(0) {}
     __device__ __forceinline__ void add(uint32_t v) {
-        asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.u32 %2, %2, 0;"
-            : "+r"(l0), "+r"(l1), "+r"(h) : "r"(v));
+        asm("add.cc.u64 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+l"(lo), "+r"(h) : "l"((uint64_t)v));
     }
     __device__ __forceinline__ void mad(uint32_t a, uint32_t x) {
-        asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\tmadc.hi.cc.u32 %1, %3, %4, %1;\n\taddc.u32 %2, %2, 0;"
-            : "+r"(l0), "+r"(l1), "+r"(h) : "r"(a), "r"(x));
+        asm("{\n\t.reg .u64 p;\n\tmul.wide.u32 p, %2, %3;\n\tadd.cc.u64 %0, %0, p;\n\taddc.u32 %1, %1, 0;\n\t}"
+            : "+l"(lo), "+r"(h) : "r"(a), "r"(x));
     }
-    __device__ __forceinline__ uint32_t reduce(const DevMod &M) const {
-        return mod96(h, ((uint64_t)l1 << 32) | l0, M);
-    }
+    __device__ __forceinline__ uint32_t reduce(const DevMod &M) const { return mod96(h, lo, M); }
 };
 
 // y' = (alpha*r + beta*y) mod m; alpha, beta already reduced mod m; beta == 0

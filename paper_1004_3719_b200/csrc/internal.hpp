@@ -68,6 +68,8 @@ struct DevMod {
     uint32_t vbytes;     // bytes per stored value (1, 2, 4)
     uint64_t mu;         // floor(2^64 / m)
     uint64_t r64;        // 2^64 mod m
+    uint32_t mu32;       // floor(2^32 / m) (used when m <= 2^16)
+    uint32_t pad_;
 };
 
 // Device view of one packed operator (A or A^T).

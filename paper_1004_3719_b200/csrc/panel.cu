@@ -23,12 +23,20 @@ void count_launch();
 namespace {
 
 constexpr int PANEL_THREADS = 1024;
-constexpr int PB = 8;                       // entries per stream per thread per round
-constexpr uint32_t PANEL_NONE = 0xFFFFFFFFu;  // no entry (bit 31 is never set in a packed word)
+constexpr int PB = 8;  // entries per thread per round (all loads issued first)
 
-template <class IT>
-__device__ __forceinline__ void st_partial(IT *p, uint32_t v) {
-    *p = (IT)v;
+// partial stores stay in L2 for the reduction pass
+__device__ __forceinline__ void st_keep(uint8_t *p, uint32_t v) {
+    asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(p), "h"((unsigned short)v),
+                 "l"(POLICY_EVICT_LAST));
+}
+__device__ __forceinline__ void st_keep(uint16_t *p, uint32_t v) {
+    asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(p), "h"((unsigned short)v),
+                 "l"(POLICY_EVICT_LAST));
+}
+__device__ __forceinline__ void st_keep(uint32_t *p, uint32_t v) {
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v),
+                 "l"(POLICY_EVICT_LAST));
 }
 
 // x panel -> shared memory, converted to the narrow staged type.
@@ -38,14 +46,16 @@ __device__ __forceinline__ void stage_x(IT *sx, const uint32_t *__restrict__ x, 
     for (uint32_t i = threadIdx.x; i < wn; i += PANEL_THREADS) sx[i] = (IT)__ldg(x + c0 + i);
 }
 
+// Addend of one packed entry, < m.  +-1 entries: x or m - x (0 stays 0);
+// valued entries: (a * x) mod m, in 32-bit arithmetic when m <= 2^16.
 template <bool SPLIT>
-__device__ __forceinline__ void acc_add(uint32_t *acc, uint32_t R, uint32_t row, uint32_t v) {
-    if constexpr (SPLIT) {
-        atomicAdd(acc + row, v & 0xFFFFu);
-        atomicAdd(acc + R + row, v >> 16);
-    } else {
-        atomicAdd(acc + row, v);
+__device__ __forceinline__ uint32_t addend(bool valued, uint32_t w, uint32_t a, uint32_t xv,
+                                           const DevMod &M) {
+    if (valued) {
+        if constexpr (SPLIT) return mod64((uint64_t)a * xv, M);
+        else return mod32(a * xv, M);
     }
+    return (w & PANEL_SIGN) ? (xv ? M.m - xv : 0u) : xv;
 }
 
 template <class IT, bool SPLIT, class VT>
@@ -55,7 +65,6 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
     const PanelGeom g = op.g;
     IT *sx = reinterpret_cast<IT *>(smem);
     uint32_t *acc = reinterpret_cast<uint32_t *>(smem + (size_t)g.W * sizeof(IT));
-    const uint32_t m = M.m;
     const uint32_t t0 = op.cta_t0[blockIdx.x], t1 = op.cta_t0[blockIdx.x + 1];
     const VT *vval = reinterpret_cast<const VT *>(op.vval);
     for (uint32_t i = threadIdx.x; i < g.R * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
@@ -69,33 +78,36 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
             cur_p = p;
         }
         __syncthreads();
-        // One round issues every load of up to PB +-1 and PB valued entries per
-        // thread before the first shared-memory op, so a tile costs about one
-        // memory round trip (+-1 addend: x or m - x; valued: (a*x) mod m).
+        // the tile's +-1 and valued entries as one index space [0, np + nv):
+        // each round issues all PB loads of a thread before any shared op
         {
             const uint32_t p0 = op.tp[t], np = op.tp[t + 1] - p0;
             const uint32_t v0 = op.tv[t], nv = op.tv[t + 1] - v0;
-            const uint32_t nmax = max(np, nv);
-            for (uint32_t base = threadIdx.x; base < nmax; base += PB * PANEL_THREADS) {
-                uint32_t w[PB], vw[PB], va[PB];
+            const uint32_t n = np + nv;
+            const uint32_t *pw = op.pent + p0;
+            const uint32_t *vw = op.vent + v0 - np;   // index e >= np
+            const VT *va = vval + v0 - np;
+            for (uint32_t base = threadIdx.x; base < n; base += PB * PANEL_THREADS) {
+                uint32_t w[PB], a[PB];
 #pragma unroll
                 for (int u = 0; u < PB; ++u) {
                     const uint32_t e = base + u * PANEL_THREADS;
-                    w[u] = e < np ? ld_stream(op.pent + p0 + e) : PANEL_NONE;
-                    vw[u] = e < nv ? ld_stream(op.vent + v0 + e) : PANEL_NONE;
-                    va[u] = e < nv ? ld_stream(vval + v0 + e) : 0u;
+                    w[u] = e < np ? ld_stream(pw + e) : e < n ? ld_stream(vw + e) : 0u;
+                    a[u] = (e >= np && e < n) ? ld_stream(va + e) : 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < PB; ++u) {
-                    if (w[u] != PANEL_NONE) {
+                    const uint32_t e = base + u * PANEL_THREADS;
+                    if (e < n) {
                         const uint32_t xv = sx[w[u] & 0xFFFFu];
-                        const uint32_t a = (w[u] & PANEL_SIGN) ? (xv ? m - xv : 0u) : xv;
-                        acc_add<SPLIT>(acc, g.R, w[u] >> PANEL_ROW_SHIFT, a);
-                    }
-                    if (vw[u] != PANEL_NONE) {
-                        const uint32_t xv = sx[vw[u] & 0xFFFFu];
-                        acc_add<SPLIT>(acc, g.R, vw[u] >> PANEL_ROW_SHIFT,
-                                       mod64((uint64_t)va[u] * xv, M));
+                        const uint32_t ad = addend<SPLIT>(e >= np, w[u], a[u], xv, M);
+                        const uint32_t row = w[u] >> PANEL_ROW_SHIFT;
+                        if constexpr (SPLIT) {
+                            atomicAdd(acc + row, ad & 0xFFFFu);
+                            atomicAdd(acc + g.R + row, ad >> 16);
+                        } else {
+                            atomicAdd(acc + row, ad);
+                        }
                     }
                 }
             }
@@ -106,31 +118,58 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
         const uint32_t rn = (uint32_t)min((uint64_t)g.R, (uint64_t)op.rows - r0);
         IT *out = partial + (uint64_t)p * op.rows + r0;
         for (uint32_t r = threadIdx.x; r < rn; r += PANEL_THREADS) {
-            uint64_t s = acc[r];
-            acc[r] = 0;
+            uint32_t res;
             if constexpr (SPLIT) {
-                s += (uint64_t)acc[g.R + r] << 16;
+                // lo, hi < 2^30 (<= W = 2^14 addends each): exact in u64
+                res = mod64((uint64_t)acc[r] + ((uint64_t)acc[g.R + r] << 16), M);
                 acc[g.R + r] = 0;
+            } else {
+                res = mod32(acc[r], M);   // < W * m <= 2^32 for m <= 2^16
             }
-            st_partial(out + r, mod64(s, M));
+            acc[r] = 0;
+            st_keep(out + r, res);
         }
         // the next tile's __syncthreads orders these writes before reuse
     }
 }
 
-template <class IT>
+// y[r] = alpha * sum_p partial[p][r] + beta * y[r]; VEC consecutive rows per
+// thread so each panel's partials load as one vector.
+template <class IT, int VEC>
 __global__ void k_panel_reduce(const IT *__restrict__ partial, uint32_t P, uint32_t rows,
                                DevMod M, uint32_t alpha, uint32_t beta, uint32_t *__restrict__ y) {
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-        uint64_t s = 0;  // P residues < m: < 2^64 for any P < 2^32
-        uint32_t p = 0;
-        for (; p + 4 <= P; p += 4) {
-            uint32_t v0 = partial[(uint64_t)p * rows + r], v1 = partial[(uint64_t)(p + 1) * rows + r];
-            uint32_t v2 = partial[(uint64_t)(p + 2) * rows + r], v3 = partial[(uint64_t)(p + 3) * rows + r];
-            s += (uint64_t)v0 + v1 + v2 + v3;
+    const uint32_t nvec = rows / VEC;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
+        uint64_t s[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) s[i] = 0;
+        for (uint32_t p = 0; p < P; ++p) {
+            const IT *src = partial + (uint64_t)p * rows + (uint64_t)v * VEC;
+            IT e[VEC];
+            if constexpr (VEC * sizeof(IT) == 16) {
+                *reinterpret_cast<uint4 *>(e) = *reinterpret_cast<const uint4 *>(src);
+            } else if constexpr (VEC * sizeof(IT) == 8) {
+                *reinterpret_cast<uint2 *>(e) = *reinterpret_cast<const uint2 *>(src);
+            } else {
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) e[i] = src[i];
+            }
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) s[i] += e[i];
         }
-        for (; p < P; ++p) s += partial[(uint64_t)p * rows + r];
-        uint32_t yold = beta ? y[r] : 0u;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            const uint32_t r = v * VEC + i;
+            const uint32_t yold = beta ? y[r] : 0u;
+            y[r] = epilogue(mod64(s[i], M), alpha, beta, yold, M);
+        }
+    }
+    // ragged tail (rows % VEC), handled by the first threads
+    const uint32_t r = nvec * VEC + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < rows && blockIdx.x * blockDim.x + threadIdx.x < VEC) {
+        uint64_t s = 0;
+        for (uint32_t p = 0; p < P; ++p) s += partial[(uint64_t)p * rows + r];
+        const uint32_t yold = beta ? y[r] : 0u;
         y[r] = epilogue(mod64(s, M), alpha, beta, yold, M);
     }
 }
@@ -160,8 +199,15 @@ int launch_t(const DevPanel &op, const DevMod &M, uint32_t alpha, const uint32_t
         if (e) return e;
     }
     if (op.rows) {
-        uint32_t blocks = std::min<uint32_t>((op.rows + 255) / 256, g.nctas * 8);
-        k_panel_reduce<IT><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
+        // the partial rows are 16-byte aligned per panel only if rows % VEC == 0
+        constexpr int VEC = 16 / sizeof(IT);
+        const bool vec_ok = (op.rows % VEC) == 0;
+        const uint32_t work = vec_ok ? op.rows / VEC : op.rows;
+        const uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((work + 255) / 256, g.nctas * 8));
+        if (vec_ok)
+            k_panel_reduce<IT, VEC><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
+        else
+            k_panel_reduce<IT, 1><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
         count_launch();
     }
     return (int)cudaGetLastError();
@@ -175,9 +221,7 @@ int launch_panel_apply(const DevPanel &op, const DevMod &M, uint32_t alpha, cons
     switch (op.g.xbytes) {
         case 1: return launch_t<uint8_t, false>(op, M, alpha, x, beta, y, st);
         case 2: return launch_t<uint16_t, false>(op, M, alpha, x, beta, y, st);
-        default:
-            if (op.g.split) return launch_t<uint32_t, true>(op, M, alpha, x, beta, y, st);
-            return launch_t<uint32_t, false>(op, M, alpha, x, beta, y, st);
+        default: return launch_t<uint32_t, true>(op, M, alpha, x, beta, y, st);
     }
 }
 

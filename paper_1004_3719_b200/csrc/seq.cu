@@ -169,7 +169,7 @@ k_seq_step(DevOp op, DevMod M, uint32_t k, uint32_t ku, const IT *__restrict__ V
     if (part_prev) finalize_pairs(part_prev, nprev, pairs, gw, nw, lane, M, S_prev);
     SeqOut<IT, KUP, PAcc> out{Vout, Uc, k};
     const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
-    for (uint32_t w = gw; w < items; w += nw) block_item<VT, KP>(op, M, w, lane, k, Vin, k, out);
+    for (uint32_t w = gw; w < items; w += nw) block_item<VT, KP, 8>(op, M, w, lane, k, Vin, k, out);
     // lanes g*KP + cl hold partials of column cl: sum the groups, then the warps
 #pragma unroll
     for (int a = 0; a < KUP; ++a) {
