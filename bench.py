@@ -87,7 +87,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.nv:
@@ -120,10 +120,16 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
 
 
+LAUNCHES = {"timed": 0}
+
+
 def timed_steps(step_fns, steps, warmup, flush, stream):
     """Run warmup + steps of a list of launch closures.  Returns per-launch
-    event times (ms, shape steps x len(step_fns)) and total step times."""
+    event times (ms, shape steps x len(step_fns)); LAUNCHES["timed"] gets the
+    number of library kernels launched inside the timed steps."""
     import torch
+
+    import paper_1004_3719_b200 as ff
     for _ in range(warmup):
         flush.zero_()
         for f in step_fns:
@@ -131,12 +137,14 @@ def timed_steps(step_fns, steps, warmup, flush, stream):
     torch.cuda.synchronize()
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in step_fns] for _ in range(steps)]
+    l0 = ff.ffspmv_kernel_launches()
     for s in range(steps):
         flush.zero_()
         for j, f in enumerate(step_fns):
             ev[s][j][0].record(stream)
             f()
             ev[s][j][1].record(stream)
+    LAUNCHES["timed"] = ff.ffspmv_kernel_launches() - l0
     torch.cuda.synchronize()
     t = np.array([[a.elapsed_time(b) for a, b in row] for row in ev])
     return t
@@ -177,10 +185,9 @@ def bench_ours(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    launches0 = ff.ffspmv_kernel_launches()
     with ClockSampler(local) as clk:
         t = timed_steps(fns, args.steps, args.warmup, flush, stream)
-    launches = ff.ffspmv_kernel_launches() - launches0 - len(fns) * args.warmup
+    launches = LAUNCHES["timed"]
     torch.cuda.synchronize()
     step_ms = float(t.sum(axis=1).mean())
     total_ms = float(t.sum())
@@ -192,11 +199,14 @@ def bench_ours(args):
     units_per_step = 2 * info["nnz"]             # apply + transpose
     value = units_per_step * world * args.steps / (total_ms / 1e3)
     alg = info["alg_bytes_apply"] + info["alg_bytes_transpose"]
-    kern_ms = float(t.sum(axis=1).mean())        # both launches are k_apply
+    kern_ms = float(t.sum(axis=1).mean())        # the two apply calls of a step
     achieved = alg / (kern_ms / 1e3) / 1e9
+    panels = info["strategy_apply"] == ff.STRATEGY_PANELS
+    kname = ("k_panel + k_panel_reduce (x panels in shared memory; A and A^T calls)" if panels
+             else "k_apply (rows layout; A and A^T calls)")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": ncu_traffic(f"{cfg}_apply"),
-                "kernel": "k_apply<uint16_t> (A and A^T launches)", "peak_source": peak_src,
+                "kernel": kname, "peak_source": peak_src,
                 "alg_bytes_per_step": alg,
                 "apply_ms": round(float(t[:, 0].mean()), 5),
                 "transpose_ms": round(float(t[:, 1].mean()), 5)}
@@ -213,9 +223,11 @@ def bench_ours(args):
            "mflops_paper_unit": 2 * value / 1e6}
     out["clocks"] = clk.summary()
     out["e2e"] = _e2e(ff, A, M, args, rows, cols, m, g, world)
-    out["plan"] = {k: info[k] for k in ("bands", "bands_sell", "bands_csr", "bands_coos", "slices",
-                                        "long_rows", "nnz_pm1", "nnz_valued", "padded_slots",
-                                        "stream_bytes", "create_seconds")}
+    out["plan"] = {k: info[k] for k in ("strategy_apply", "strategy_transpose", "panels",
+                                        "panel_bands", "gather_locality", "bands", "bands_sell",
+                                        "bands_csr", "bands_coos", "slices", "long_rows", "nnz_pm1",
+                                        "nnz_valued", "padded_slots", "stream_bytes",
+                                        "panel_stream_bytes", "create_seconds")}
     if rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(M, budget_s=args.cpu_seconds)
         if not args.no_extras:
@@ -327,15 +339,16 @@ def extras(ff, flush, stream, hbm_peak, args):
     g = synth.rng(2003)
     x = to_dev(synth.uniform(g, M["cols"], M["m"]))
     y = torch.empty(M["rows"], dtype=torch.int32, device="cuda")
-    t = timed_steps([lambda: ff.ffspmv_apply(A, 1, x, 0, y, stream)], args.steps, args.warmup,
-                    flush, stream)
+    t = timed_steps([lambda: ff.ffspmv_apply(A, 1, x, 0, y, stream)], min(args.steps, 50),
+                    args.warmup, flush, stream)
     ms = float(t.mean())
     res["c3_apply"] = {"nnz_per_s": info["nnz"] / (ms / 1e3), "ms": ms,
                        "alg_gbs": info["alg_bytes_apply"] / (ms / 1e3) / 1e9,
                        "frac": info["alg_bytes_apply"] / (ms / 1e3) / 1e9 / hbm_peak,
                        "stream_gbs": (info["stream_bytes"] + 4 * (M["rows"] + M["cols"])) / (ms / 1e3) / 1e9,
                        "traffic": ncu_traffic("c3_apply"),
-                       "plan": {k: info[k] for k in ("bands_sell", "bands_csr", "bands_coos",
+                       "plan": {k: info[k] for k in ("strategy_apply", "panels", "panel_bands",
+                                                     "bands_sell", "bands_csr", "bands_coos",
                                                      "long_rows", "slices", "padded_slots")}}
     del A, x, y, M
     # c4: block SpMM, m = 2^31 - 1
@@ -346,8 +359,8 @@ def extras(ff, flush, stream, hbm_peak, args):
     for k in (8, 16, 32):
         X = to_dev(synth.uniform(g, (M["cols"], k), M["m"]))
         Y = torch.empty((M["rows"], k), dtype=torch.int32, device="cuda")
-        t = timed_steps([lambda: ff.ffspmv_apply_block(A, k, 1, X, 0, Y, stream)], args.steps,
-                        args.warmup, flush, stream)
+        t = timed_steps([lambda: ff.ffspmv_apply_block(A, k, 1, X, 0, Y, stream)],
+                        min(args.steps, 20), args.warmup, flush, stream)
         ms = float(t.mean())
         alg = (info["alg_bytes_apply"] - 4 * (M["rows"] + M["cols"])) + 4 * k * (M["rows"] + M["cols"])
         res[f"c4_block_k{k}"] = {"nnz_per_s": info["nnz"] / (ms / 1e3),
@@ -430,7 +443,7 @@ def bench_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c2", "c3"])

@@ -141,12 +141,11 @@ ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
     d.rows = h.rows;
     d.cols = h.cols;
     d.g = h.g;
-    void *p_tp, *p_tv, *p_pent, *p_vent, *p_vval, *p_cta, *p_part;
+    void *p_tp, *p_tv, *p_pent, *p_vval, *p_cta, *p_part;
     Part parts[] = {
         {h.tp.data(), h.tp.size() * 4, &p_tp},
         {h.tv.data(), h.tv.size() * 4, &p_tv},
         {h.pent.data(), h.pent.size() * 4, &p_pent},
-        {h.vent.data(), h.vent.size() * 4, &p_vent},
         {h.vval.data(), h.vval.size(), &p_vval},
         {h.cta_t0.data(), h.cta_t0.size() * 4, &p_cta},
         {nullptr, (size_t)h.g.P * h.rows * h.g.xbytes, &p_part},
@@ -170,7 +169,7 @@ ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
     d.tp = (const uint32_t *)p_tp;
     d.tv = (const uint32_t *)p_tv;
     d.pent = (const uint32_t *)p_pent;
-    d.vent = (const uint32_t *)p_vent;
+    d.vent = nullptr;
     d.vval = p_vval;
     d.cta_t0 = (const uint32_t *)p_cta;
     d.partial = p_part;
@@ -210,8 +209,8 @@ ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &devic
         if (o->strategy < 0 || o->strategy > 2)
             return fail(FFSPMV_ERR_INVALID_ARG, "strategy must be 0, 1 or 2");
         bo.strategy = o->strategy;
-        if (o->panel_rows && (o->panel_rows > 16384 || o->panel_rows % 32))
-            return fail(FFSPMV_ERR_INVALID_ARG, "panel_rows must be a multiple of 32 <= 16384");
+        if (o->panel_rows && (o->panel_rows > PANEL_R_DEFAULT || o->panel_rows % 32))
+            return fail(FFSPMV_ERR_INVALID_ARG, "panel_rows must be a multiple of 32 <= 16320");
         if (o->panel_cols && (o->panel_cols > 65536 || o->panel_cols % 32))
             return fail(FFSPMV_ERR_INVALID_ARG, "panel_cols must be a multiple of 32 <= 65536");
         bo.panel_rows = o->panel_rows;

@@ -137,6 +137,10 @@ struct Canon;
 constexpr uint32_t PANEL_COL_BITS = 16;
 constexpr uint32_t PANEL_SIGN = 1u << 16;
 constexpr uint32_t PANEL_ROW_SHIFT = 17;
+// Band rows: 14-bit row field, the top 64 slots are per-lane dummies that
+// absorb the masked-off lanes of a round without a branch.
+constexpr uint32_t PANEL_R_DEFAULT = 16384u - 64u;
+constexpr uint32_t PANEL_DUMMY_ROW = 16384u - 64u;
 
 struct PanelGeom {
     uint32_t W = 0, R = 0, P = 0, B = 0;
@@ -148,9 +152,9 @@ struct PanelGeom {
 struct HostPanel {
     uint32_t rows = 0, cols = 0;
     PanelGeom g;
-    std::vector<uint32_t> tp, tv;      // tile offsets, P*B + 1 each
-    std::vector<uint32_t> pent, vent;  // packed entries
-    std::vector<uint8_t> vval;         // values of vent (vbytes each)
+    std::vector<uint32_t> tp, tv;      // tile entry / value offsets, P*B + 1 each
+    std::vector<uint32_t> pent, vent;  // pent: packed entries (per tile: +-1 then valued); vent unused
+    std::vector<uint8_t> vval;         // values of the valued entries (vbytes each)
     std::vector<uint32_t> cta_t0;      // nctas + 1 tile boundaries
     uint64_t nnz_pm = 0, nnz_val = 0, stream_bytes = 0;
 };

@@ -24,6 +24,7 @@ namespace {
 
 constexpr int PANEL_THREADS = 1024;
 constexpr int PB = 8;  // entries per thread per round (all loads issued first)
+constexpr uint32_t ACC_STRIDE = 16384;  // accumulator slots incl. the 64 per-lane dummies
 
 // partial stores stay in L2 for the reduction pass
 __device__ __forceinline__ void st_keep(uint8_t *p, uint32_t v) {
@@ -67,7 +68,7 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
     uint32_t *acc = reinterpret_cast<uint32_t *>(smem + (size_t)g.W * sizeof(IT));
     const uint32_t t0 = op.cta_t0[blockIdx.x], t1 = op.cta_t0[blockIdx.x + 1];
     const VT *vval = reinterpret_cast<const VT *>(op.vval);
-    for (uint32_t i = threadIdx.x; i < g.R * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
+    for (uint32_t i = threadIdx.x; i < ACC_STRIDE * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
     uint32_t cur_p = 0xFFFFFFFFu;
     for (uint32_t t = t0; t < t1; ++t) {
         const uint32_t p = t / g.B, b = t - p * g.B;
@@ -80,34 +81,33 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
         __syncthreads();
         // the tile's +-1 and valued entries as one index space [0, np + nv):
         // each round issues all PB loads of a thread before any shared op
+        // Masked-off lanes read a per-lane dummy word (row PANEL_DUMMY_ROW +
+        // lane, value 0) so the steady state has no branch.
         {
-            const uint32_t p0 = op.tp[t], np = op.tp[t + 1] - p0;
-            const uint32_t v0 = op.tv[t], nv = op.tv[t + 1] - v0;
-            const uint32_t n = np + nv;
-            const uint32_t *pw = op.pent + p0;
-            const uint32_t *vw = op.vent + v0 - np;   // index e >= np
-            const VT *va = vval + v0 - np;
+            const uint32_t e0 = op.tp[t], n = op.tp[t + 1] - e0;
+            const uint32_t v0 = op.tv[t], np = n - (op.tv[t + 1] - v0);
+            const uint32_t *ent = op.pent + e0;
+            const VT *va = vval + v0 - np;            // value of entry e >= np
+            const uint32_t dummy = (PANEL_DUMMY_ROW + (threadIdx.x & 31)) << PANEL_ROW_SHIFT;
             for (uint32_t base = threadIdx.x; base < n; base += PB * PANEL_THREADS) {
                 uint32_t w[PB], a[PB];
 #pragma unroll
                 for (int u = 0; u < PB; ++u) {
                     const uint32_t e = base + u * PANEL_THREADS;
-                    w[u] = e < np ? ld_stream(pw + e) : e < n ? ld_stream(vw + e) : 0u;
+                    w[u] = e < n ? ld_stream(ent + e) : dummy;
                     a[u] = (e >= np && e < n) ? ld_stream(va + e) : 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < PB; ++u) {
                     const uint32_t e = base + u * PANEL_THREADS;
-                    if (e < n) {
-                        const uint32_t xv = sx[w[u] & 0xFFFFu];
-                        const uint32_t ad = addend<SPLIT>(e >= np, w[u], a[u], xv, M);
-                        const uint32_t row = w[u] >> PANEL_ROW_SHIFT;
-                        if constexpr (SPLIT) {
-                            atomicAdd(acc + row, ad & 0xFFFFu);
-                            atomicAdd(acc + g.R + row, ad >> 16);
-                        } else {
-                            atomicAdd(acc + row, ad);
-                        }
+                    const uint32_t xv = sx[w[u] & 0xFFFFu];
+                    const uint32_t ad = addend<SPLIT>(e >= np, w[u], a[u], xv, M);
+                    const uint32_t row = w[u] >> PANEL_ROW_SHIFT;
+                    if constexpr (SPLIT) {
+                        atomicAdd(acc + row, ad & 0xFFFFu);
+                        atomicAdd(acc + ACC_STRIDE + row, ad >> 16);
+                    } else {
+                        atomicAdd(acc + row, ad);
                     }
                 }
             }
@@ -121,8 +121,8 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
             uint32_t res;
             if constexpr (SPLIT) {
                 // lo, hi < 2^30 (<= W = 2^14 addends each): exact in u64
-                res = mod64((uint64_t)acc[r] + ((uint64_t)acc[g.R + r] << 16), M);
-                acc[g.R + r] = 0;
+                res = mod64((uint64_t)acc[r] + ((uint64_t)acc[ACC_STRIDE + r] << 16), M);
+                acc[ACC_STRIDE + r] = 0;
             } else {
                 res = mod32(acc[r], M);   // < W * m <= 2^32 for m <= 2^16
             }
@@ -180,7 +180,7 @@ int launch_t(const DevPanel &op, const DevMod &M, uint32_t alpha, const uint32_t
     const PanelGeom &g = op.g;
     IT *partial = reinterpret_cast<IT *>(op.partial);
     if (g.P > 0 && g.B > 0) {
-        size_t smem = (size_t)g.W * sizeof(IT) + (size_t)g.R * 4 * (SPLIT ? 2 : 1);
+        size_t smem = (size_t)g.W * sizeof(IT) + (size_t)ACC_STRIDE * 4 * (SPLIT ? 2 : 1);
         auto run = [&](auto kern) {
             static size_t configured = 0;   // per instantiation
             if (configured < smem) {

@@ -15,7 +15,7 @@ PanelGeom panel_geometry(uint64_t rows, uint64_t cols, uint32_t m, const BuildOp
     g.split = m > 65536u ? 1 : 0;
     // smem: W * xbytes (x panel) + R * 4 * (1 + split) (accumulators) <= 192 KB
     g.W = g.xbytes == 4 ? 16384u : 65536u;
-    g.R = 16384u;
+    g.R = PANEL_R_DEFAULT;
     if (bo.panel_cols) g.W = std::min<uint32_t>(bo.panel_cols, g.W);
     if (bo.panel_rows) g.R = std::min<uint32_t>(bo.panel_rows, g.R);
     g.P = (uint32_t)((cols + g.W - 1) / g.W);
@@ -39,24 +39,28 @@ void pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &
     auto is_pm = [&](uint32_t v) { return seg && (v == 1u || (m > 2 && v == m - 1)); };
 
     // counting sort of the entries by tile (rows visited in order -> each
-    // tile's entries come out sorted by (row, col))
+    // tile's entries come out sorted by (row, col)).  Tile t occupies
+    // ent[tp[t], tp[t+1]): its +-1 entries first, then its valued entries,
+    // whose values are vval[tv[t] ...] in the same order.
     hp.tp.assign(T + 1, 0);
     hp.tv.assign(T + 1, 0);
+    std::vector<uint32_t> npm(T, 0);
     for (uint64_t r = 0; r < a.nrows; ++r) {
         uint64_t b = r / g.R;
         for (uint64_t t = a.ptr[r]; t < a.ptr[r + 1]; ++t) {
             uint64_t tile = (uint64_t)(a.idx[t] / g.W) * g.B + b;
-            if (is_pm(a.val[t])) hp.tp[tile + 1]++;
+            hp.tp[tile + 1]++;
+            if (is_pm(a.val[t])) npm[tile]++;
             else hp.tv[tile + 1]++;
         }
     }
     for (uint64_t t = 0; t < T; ++t) { hp.tp[t + 1] += hp.tp[t]; hp.tv[t + 1] += hp.tv[t]; }
-    hp.nnz_pm = hp.tp[T];
     hp.nnz_val = hp.tv[T];
-    hp.pent.resize(hp.nnz_pm);
-    hp.vent.resize(hp.nnz_val);
+    hp.nnz_pm = hp.tp[T] - hp.nnz_val;
+    hp.pent.resize(hp.tp[T]);
     hp.vval.resize(hp.nnz_val * vb);
-    std::vector<uint32_t> pp(hp.tp.begin(), hp.tp.end() - 1), pv(hp.tv.begin(), hp.tv.end() - 1);
+    std::vector<uint32_t> pp(T), pv(T), pvv(T);
+    for (uint64_t t = 0; t < T; ++t) { pp[t] = hp.tp[t]; pv[t] = hp.tp[t] + npm[t]; pvv[t] = hp.tv[t]; }
     for (uint64_t r = 0; r < a.nrows; ++r) {
         uint64_t b = r / g.R;
         uint32_t rl = (uint32_t)(r - b * g.R) << PANEL_ROW_SHIFT;
@@ -68,9 +72,8 @@ void pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &
             if (is_pm(v)) {
                 hp.pent[pp[tile]++] = word | (v == 1u ? 0u : PANEL_SIGN);
             } else {
-                uint32_t i = pv[tile]++;
-                hp.vent[i] = word;
-                std::memcpy(&hp.vval[(uint64_t)i * vb], &v, vb);
+                hp.pent[pv[tile]++] = word;
+                std::memcpy(&hp.vval[(uint64_t)(pvv[tile]++) * vb], &v, vb);
             }
         }
     }
@@ -80,7 +83,7 @@ void pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &
     std::vector<double> cost(T);
     double total = 0;
     for (uint64_t t = 0; t < T; ++t) {
-        uint64_t e = (hp.tp[t + 1] - hp.tp[t]) + (hp.tv[t + 1] - hp.tv[t]);
+        uint64_t e = hp.tp[t + 1] - hp.tp[t];
         uint64_t b = t % g.B;
         uint64_t rn = std::min<uint64_t>(g.R, a.nrows - b * g.R);
         cost[t] = (double)e + 0.5 * (double)rn;
@@ -96,6 +99,7 @@ void pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &
     }
     for (; c < g.nctas; ++c) hp.cta_t0[c] = (uint32_t)T;
     hp.stream_bytes = hp.nnz_pm * 4 + hp.nnz_val * (4ull + vb) + (T + 1) * 8;
+    hp.vent.clear();
 }
 
 uint64_t reconstruct_panels(const HostPanel &hp, uint32_t m, uint32_t vb, uint32_t *rr,
@@ -108,14 +112,16 @@ uint64_t reconstruct_panels(const HostPanel &hp, uint32_t m, uint32_t vb, uint32
     const PanelGeom &g = hp.g;
     for (uint64_t t = 0; t < (uint64_t)g.P * g.B; ++t) {
         uint64_t p = t / g.B, b = t % g.B;
+        const uint32_t nv = hp.tv[t + 1] - hp.tv[t], np = hp.tp[t + 1] - hp.tp[t] - nv;
         for (uint32_t e = hp.tp[t]; e < hp.tp[t + 1]; ++e) {
-            uint32_t w = hp.pent[e];
-            emit((uint32_t)(b * g.R + (w >> PANEL_ROW_SHIFT)), (uint32_t)(p * g.W + (w & 0xFFFFu)),
-                 (w & PANEL_SIGN) ? m - 1 : 1u);
-        }
-        for (uint32_t e = hp.tv[t]; e < hp.tv[t + 1]; ++e) {
-            uint32_t w = hp.vent[e], v = 0;
-            std::memcpy(&v, &hp.vval[(uint64_t)e * vb], vb);
+            const uint32_t w = hp.pent[e], j = e - hp.tp[t];
+            uint32_t v;
+            if (j < np) {
+                v = (w & PANEL_SIGN) ? m - 1 : 1u;
+            } else {
+                v = 0;
+                std::memcpy(&v, &hp.vval[(uint64_t)(hp.tv[t] + j - np) * vb], vb);
+            }
             emit((uint32_t)(b * g.R + (w >> PANEL_ROW_SHIFT)), (uint32_t)(p * g.W + (w & 0xFFFFu)), v);
         }
     }
