@@ -76,7 +76,6 @@ __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, ui
     for (uint32_t c0 = 0; c0 < k; c0 += KP) {
         const uint32_t col = c0 + cl;
         const bool colok = col < k;
-        const TX *Xc = X + col;
 #pragma unroll 1
         for (int pass = 0; pass < S::PASSES; ++pass) {
             const uint32_t rbase = pass * S::G * S::NR + g;
@@ -90,7 +89,9 @@ __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, ui
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i) {
                     cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
-                    xv[i] = (cs[i] != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (size_t)((cs[i] & COL_MASK) * ldx)) : 0u;
+                    // 32-bit element index, one IMAD.WIDE for the address
+                    const uint32_t idx = (cs[i] & COL_MASK) * ldx + col;
+                    xv[i] = (cs[i] != PAD_COL && colok) ? (uint32_t)ld_gather(X + idx) : 0u;
                 }
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i) acc[i].add((cs[i] & SIGN_BIT) ? m - xv[i] : xv[i]);
@@ -106,7 +107,8 @@ __device__ __forceinline__ void block_slice(const DevOp &op, const DevMod &M, ui
                 for (int i = 0; i < S::NR; ++i) {
                     const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
                     as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i * S::G);
-                    xv[i] = (c != PAD_COL && colok) ? (uint32_t)ld_gather(Xc + (size_t)(c * ldx)) : 0u;
+                    const uint32_t idx = c * ldx + col;
+                    xv[i] = (c != PAD_COL && colok) ? (uint32_t)ld_gather(X + idx) : 0u;
                 }
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i) acc[i].mad(as[i], xv[i]);
