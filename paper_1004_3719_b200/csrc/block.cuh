@@ -233,10 +233,140 @@ k_block(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint32_t ldx, 
     block_item<VT, KP, 16>(op, M, w, threadIdx.x & 31, k, X, ldx, out);
 }
 
+// ---------------------------------------------------- vectorised columns ---
+// CPL consecutive columns per lane: one 8 / 16-byte gather of X per (row,
+// slot) feeds CPL accumulators, so the per-gather index / address / shuffle /
+// predicate work is shared by CPL columns.  Requires k % CPL == 0, ldx % CPL
+// == 0 and an aligned X (checked on the host).
+template <class TX, int CPL> struct VecT;
+template <> struct VecT<uint32_t, 4> { typedef uint4 T; };
+template <> struct VecT<uint32_t, 2> { typedef uint2 T; };
+template <> struct VecT<uint16_t, 4> { typedef uint2 T; };
+template <> struct VecT<uint16_t, 2> { typedef uint32_t T; };
+
+template <class TX, int CPL>
+__device__ __forceinline__ void ld_vec(const TX *p, uint32_t (&v)[CPL]) {
+    typedef typename VecT<TX, CPL>::T V;
+    const V w = __ldg(reinterpret_cast<const V *>(p));
+    const uint32_t *u = reinterpret_cast<const uint32_t *>(&w);
+    if constexpr (sizeof(TX) == 4) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) v[c] = u[c];
+    } else {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) v[c] = (u[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+    }
+}
+
+template <class Acc, class VT, int KPV, int NRMAX, int CPL, class TX, class Out>
+__device__ __forceinline__ void block_slice_vec(const DevOp &op, const DevMod &M, uint32_t s,
+                                                const SliceHdr &h, uint32_t lane, uint32_t k,
+                                                const TX *__restrict__ X, uint32_t ldx,
+                                                Out &out) {
+    using S = SliceShape<KPV, NRMAX>;
+    const uint32_t g = lane / KPV, cl = lane % KPV;
+    const uint32_t m = M.m;
+    const uint32_t *pc = op.pcol + h.off_p + lane;
+    const uint32_t *vc = op.vcol + h.off_v + lane;
+    const VT *vv = reinterpret_cast<const VT *>(op.vval) + h.off_v + lane;
+    const uint32_t wp = h.wp, wv = h.wv;
+    for (uint32_t c0 = 0; c0 < k; c0 += KPV * CPL) {
+        const uint32_t col = c0 + cl * CPL;
+        const bool colok = col < k;
+#pragma unroll 1
+        for (int pass = 0; pass < S::PASSES; ++pass) {
+            const uint32_t rbase = pass * S::G * S::NR + g;
+            Acc acc[S::NR][CPL];
+            uint32_t cw = wp ? ld_bcast(pc) : PAD_COL;
+            for (uint32_t j = 0; j < wp; ++j) {
+                const uint32_t cur = cw;
+                if (j + 1 < wp) cw = ld_bcast(pc + (j + 1) * 32);
+                uint32_t xv[S::NR][CPL], cs[S::NR];
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i) {
+                    cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
+                    if (cs[i] != PAD_COL && colok) {
+                        ld_vec<TX, CPL>(X + ((cs[i] & COL_MASK) * ldx + col), xv[i]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) xv[i][c] = 0;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i)
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c)
+                        acc[i][c].add((cs[i] & SIGN_BIT) ? m - xv[i][c] : xv[i][c]);
+            }
+            uint32_t vw = wv ? ld_bcast(vc) : PAD_COL;
+            uint32_t aw = wv ? ld_bcast(vv) : 0u;
+            for (uint32_t j = 0; j < wv; ++j) {
+                const uint32_t cur = vw, cura = aw;
+                if (j + 1 < wv) { vw = ld_bcast(vc + (j + 1) * 32); aw = ld_bcast(vv + (j + 1) * 32); }
+                uint32_t xv[S::NR][CPL], as[S::NR];
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i) {
+                    const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
+                    as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i * S::G);
+                    if (c != PAD_COL && colok) {
+                        ld_vec<TX, CPL>(X + (c * ldx + col), xv[i]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) xv[i][q] = 0;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < S::NR; ++i)
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) acc[i][c].mad(as[i], xv[i][c]);
+            }
+#pragma unroll
+            for (int i = 0; i < S::NR; ++i) {
+                const uint32_t r = rbase + i * S::G;
+                if (r < h.nrows) {
+                    const uint32_t row = op.perm[s * 32 + r];
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) out.put(row, col + c, colok, acc[i][c].reduce(M), M);
+                }
+            }
+        }
+    }
+}
+
+// Vector kernel: slices take the CPL path with KPV lanes per row; the rare
+// long rows / CSR groups / zero rows keep the scalar path (KP lanes per row).
+template <class VT, int KPV, int CPL, int KP, class TX, class TY>
+__global__ void __launch_bounds__(BWARPS * 32)
+k_block_vec(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint32_t ldx,
+            BlockOut<TY> out) {
+    uint32_t w = blockIdx.x * BWARPS + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31;
+    if (w >= op.n_long && w - op.n_long < op.n_slices) {
+        const uint32_t s = w - op.n_long;
+        const SliceHdr h = load_hdr_b(op.slices + s);
+        switch (h.regime) {
+            case ACC32: block_slice_vec<Acc32, VT, KPV, 8, CPL>(op, M, s, h, lane, k, X, ldx, out); break;
+            case ACC64: block_slice_vec<Acc64, VT, KPV, 8, CPL>(op, M, s, h, lane, k, X, ldx, out); break;
+            default: block_slice_vec<Acc96, VT, KPV, 4, CPL>(op, M, s, h, lane, k, X, ldx, out); break;
+        }
+        return;
+    }
+    block_item<VT, KP, 16>(op, M, w, lane, k, X, ldx, out);
+}
+
 template <class VT, class TX, class TY>
 static void launch_block_vt(dim3 grid, dim3 block, cudaStream_t st, const DevOp &op,
                             const DevMod &M, uint32_t k, const TX *X, uint32_t ldx,
                             BlockOut<TY> out) {
+    const bool vec4 = k >= 8 && k % 4 == 0 && ldx % 4 == 0 &&
+                      ((uintptr_t)X % (4 * sizeof(TX))) == 0;
+    if (vec4) {
+        if (k <= 8) k_block_vec<VT, 2, 4, 8, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+        else if (k <= 16) k_block_vec<VT, 4, 4, 16, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+        else if (k <= 32) k_block_vec<VT, 8, 4, 32, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+        else k_block_vec<VT, 16, 4, 32, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+        return;
+    }
     if (k <= 1) k_block<VT, 1, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
     else if (k <= 2) k_block<VT, 2, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
     else if (k <= 4) k_block<VT, 4, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
