@@ -24,7 +24,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU_SOURCES = ["kernels.cu", "block.cu", "seq.cu", "panel.cu"]
 CPP_SOURCES = ["abi.cpp", "builder.cpp", "panel_build.cpp"]
-HEADERS = ["internal.hpp", "device.cuh", "block.cuh"]
+HEADERS = ["internal.hpp", "device.cuh", "block.cuh", "seq_mma.cuh"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -23,7 +23,15 @@ void count_launch();
 namespace {
 
 constexpr int PANEL_THREADS = 1024;
-constexpr int PB = 8;  // entries per thread per round (all loads issued first)
+constexpr int PBP = 4;  // +-1 entries per thread per round (all loads issued first)
+constexpr int PBV = 6;  // valued entries per thread per round
+constexpr uint32_t PANEL_NONE = 0xFFFFFFFFu;  // no entry (bit 31 of a packed word is 0)
+
+template <bool SPLIT>
+__device__ __forceinline__ void acc_add(uint32_t *acc, uint32_t row, uint32_t v);
+
+template <class IT, int WV>
+__device__ __forceinline__ void st_keep_vec(IT *p, const uint32_t (&v)[WV]);
 constexpr uint32_t ACC_STRIDE = 16384;  // accumulator slots incl. the 64 per-lane dummies
 
 // partial stores stay in L2 for the reduction pass
@@ -38,6 +46,33 @@ __device__ __forceinline__ void st_keep(uint16_t *p, uint32_t v) {
 __device__ __forceinline__ void st_keep(uint32_t *p, uint32_t v) {
     asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v),
                  "l"(POLICY_EVICT_LAST));
+}
+
+template <bool SPLIT>
+__device__ __forceinline__ void acc_add(uint32_t *acc, uint32_t row, uint32_t v) {
+    if constexpr (SPLIT) {
+        atomicAdd(acc + row, v & 0xFFFFu);
+        atomicAdd(acc + ACC_STRIDE + row, v >> 16);
+    } else {
+        atomicAdd(acc + row, v);
+    }
+}
+
+// WV consecutive narrow partials in one 4- or 8-byte store (L2 evict_last)
+template <class IT, int WV>
+__device__ __forceinline__ void st_keep_vec(IT *p, const uint32_t (&v)[WV]) {
+    if constexpr (sizeof(IT) == 2 && WV == 4) {
+        const uint32_t lo = v[0] | (v[1] << 16), hi = v[2] | (v[3] << 16);
+        asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(lo),
+                     "r"(hi), "l"(POLICY_EVICT_LAST));
+    } else if constexpr (sizeof(IT) == 1 && WV == 4) {
+        const uint32_t w = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+        asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(w),
+                     "l"(POLICY_EVICT_LAST));
+    } else {
+#pragma unroll
+        for (int i = 0; i < WV; ++i) p[i] = (IT)v[i];
+    }
 }
 
 // x panel -> shared memory, converted to the narrow staged type.
@@ -111,31 +146,43 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
         // each round issues all PB loads of a thread before any shared op
         // Masked-off lanes read a per-lane dummy word (row PANEL_DUMMY_ROW +
         // lane, value 0) so the steady state has no branch.
+        // The +-1 part [0, np) and the valued part [np, n) advance together
+        // with their own specialised code; each round issues all loads of both
+        // before the first shared op (one memory round trip per round).
         {
             const uint32_t e0 = op.tp[t], n = op.tp[t + 1] - e0;
-            const uint32_t v0 = op.tv[t], np = n - (op.tv[t + 1] - v0);
-            const uint32_t *ent = op.pent + e0;
-            const VT *va = vval + v0 - np;            // value of entry e >= np
-            const uint32_t dummy = (PANEL_DUMMY_ROW + (threadIdx.x & 31)) << PANEL_ROW_SHIFT;
-            for (uint32_t base = threadIdx.x; base < n; base += PB * PANEL_THREADS) {
-                uint32_t w[PB], a[PB];
+            const uint32_t v0 = op.tv[t], nv = op.tv[t + 1] - v0, np = n - nv;
+            const uint32_t *pw = op.pent + e0, *vw = op.pent + e0 + np;
+            const VT *va = vval + v0;
+            const uint32_t rounds = max((np + PBP * PANEL_THREADS - 1) / (PBP * PANEL_THREADS),
+                                        (nv + PBV * PANEL_THREADS - 1) / (PBV * PANEL_THREADS));
+            const uint32_t m = M.m;
+            for (uint32_t rd = 0; rd < rounds; ++rd) {
+                uint32_t w[PBP], x[PBV], a[PBV];
 #pragma unroll
-                for (int u = 0; u < PB; ++u) {
-                    const uint32_t e = base + u * PANEL_THREADS;
-                    w[u] = e < n ? ld_stream(ent + e) : dummy;
-                    a[u] = (e >= np && e < n) ? ld_stream(va + e) : 0u;
+                for (int u = 0; u < PBP; ++u) {
+                    const uint32_t e = (rd * PBP + u) * PANEL_THREADS + threadIdx.x;
+                    w[u] = e < np ? ld_stream(pw + e) : PANEL_NONE;
                 }
 #pragma unroll
-                for (int u = 0; u < PB; ++u) {
-                    const uint32_t e = base + u * PANEL_THREADS;
-                    const uint32_t xv = sx[w[u] & 0xFFFFu];
-                    const uint32_t ad = addend<SPLIT>(e >= np, w[u], a[u], xv, M);
-                    const uint32_t row = w[u] >> PANEL_ROW_SHIFT;
-                    if constexpr (SPLIT) {
-                        atomicAdd(acc + row, ad & 0xFFFFu);
-                        atomicAdd(acc + ACC_STRIDE + row, ad >> 16);
-                    } else {
-                        atomicAdd(acc + row, ad);
+                for (int u = 0; u < PBV; ++u) {
+                    const uint32_t e = (rd * PBV + u) * PANEL_THREADS + threadIdx.x;
+                    x[u] = e < nv ? ld_stream(vw + e) : PANEL_NONE;
+                    a[u] = e < nv ? ld_stream(va + e) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < PBP; ++u) {
+                    if (w[u] != PANEL_NONE) {
+                        const uint32_t xv = sx[w[u] & 0xFFFFu];
+                        const uint32_t ad = (w[u] & PANEL_SIGN) ? (xv ? m - xv : 0u) : xv;
+                        acc_add<SPLIT>(acc, w[u] >> PANEL_ROW_SHIFT, ad);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < PBV; ++u) {
+                    if (x[u] != PANEL_NONE) {
+                        const uint32_t xv = sx[x[u] & 0xFFFFu];
+                        acc_add<SPLIT>(acc, x[u] >> PANEL_ROW_SHIFT, addend<SPLIT>(true, 0, a[u], xv, M));
                     }
                 }
             }
@@ -145,7 +192,28 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
         const uint64_t r0 = (uint64_t)b * g.R;
         const uint32_t rn = (uint32_t)min((uint64_t)g.R, (uint64_t)op.rows - r0);
         IT *out = partial + (uint64_t)p * op.rows + r0;
-        for (uint32_t r = threadIdx.x; r < rn; r += PANEL_THREADS) {
+        constexpr int WV = 16 / sizeof(IT) < 4 ? 16 / sizeof(IT) : 4;   // rows per vector store
+        const bool vec = !SPLIT && ((uintptr_t)out % (WV * sizeof(IT))) == 0;
+        uint32_t r = 0;
+        if (vec) {
+            const uint32_t nq = rn / WV;
+            for (uint32_t q = threadIdx.x; q < nq; q += PANEL_THREADS) {
+                uint32_t v[WV];
+                if constexpr (WV == 4) {
+                    const uint4 s4 = reinterpret_cast<const uint4 *>(acc)[q];
+                    reinterpret_cast<uint4 *>(acc)[q] = make_uint4(0, 0, 0, 0);
+                    v[0] = s4.x; v[1] = s4.y; v[2] = s4.z; v[3] = s4.w;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < WV; ++i) { v[i] = acc[q * WV + i]; acc[q * WV + i] = 0; }
+                }
+#pragma unroll
+                for (int i = 0; i < WV; ++i) v[i] = mod32(v[i], M);
+                st_keep_vec<IT, WV>(out + q * WV, v);
+            }
+            r = nq * WV;
+        }
+        for (r += threadIdx.x; r < rn; r += PANEL_THREADS) {
             uint32_t res;
             if constexpr (SPLIT) {
                 // lo, hi < 2^30 (<= W = 2^14 addends each): exact in u64

@@ -10,6 +10,7 @@
 #include <algorithm>
 
 #include "block.cuh"
+#include "seq_mma.cuh"
 
 namespace ffspmv {
 
@@ -208,28 +209,37 @@ struct SeqLayout {
     IT *V[2];
     IT *Uc;          // n x ku (unfused path) or n x KUP padded (fused path)
     uint32_t *partial[2];
+    uint32_t *ufrag; // tensor-core path: per slice 256 u32 of U limbs in fragment order
     size_t bytes;
 };
 
 inline uint32_t kup_for(uint32_t ku) { return ku <= 16 ? 16 : 32; }
 inline bool fused_ok(uint32_t k, uint32_t ku) { return k <= 32 && ku <= 32; }
+// tensor-core projection: u16 iterate (2 limbs), 4 | k <= 16, ku <= 16
+inline bool mma_ok(uint32_t m, uint32_t k, uint32_t ku) {
+    return m <= 65536u && k % 4 == 0 && k >= 4 && k <= 16 && ku <= 16;
+}
 constexpr uint32_t MAX_STEP_CTAS_PER_SM = 8;
 
 template <class IT>
-SeqLayout<IT> layout(void *ws, uint64_t n, uint32_t k, uint32_t ku, uint32_t nctas) {
+SeqLayout<IT> layout(void *ws, const DevOp &op, uint32_t m, uint32_t k, uint32_t ku, uint32_t nctas) {
     SeqLayout<IT> L{};
+    const uint64_t n = op.rows;
     char *p = (char *)ws;
     size_t off = 0;
-    const uint32_t ucols = fused_ok(k, ku) ? kup_for(ku) : ku;
+    const bool mma = sizeof(IT) == 2 && mma_ok(m, k, ku);
+    const uint32_t ucols = mma ? 0 : fused_ok(k, ku) ? kup_for(ku) : ku;
     const uint32_t maxc = std::max<uint32_t>(nctas, (uint32_t)num_sms() * MAX_STEP_CTAS_PER_SM);
     size_t vb = align256(n * (size_t)k * sizeof(IT));
     size_t ub = align256(n * (size_t)ucols * sizeof(IT));
     size_t pb = align256((size_t)maxc * ku * k * sizeof(uint32_t));
+    size_t fb = mma ? align256((size_t)op.n_slices * 256 * sizeof(uint32_t)) : 0;
     L.V[0] = (IT *)(p + off); off += vb;
     L.V[1] = (IT *)(p + off); off += vb;
     L.Uc = (IT *)(p + off); off += ub;
     L.partial[0] = (uint32_t *)(p + off); off += pb;
     L.partial[1] = (uint32_t *)(p + off); off += pb;
+    L.ufrag = (uint32_t *)(p + off); off += fb;
     L.bytes = off;
     return L;
 }
@@ -308,17 +318,97 @@ int launch_step(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku, const
     }
 }
 
+// ------------------------------------------------- tensor-core projection ---
+template <class VT, int KPV, int KP>
+int launch_step_mma_t(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku,
+                      const uint16_t *Vin, uint16_t *Vout, const uint32_t *U,
+                      const uint32_t *ufrag, uint32_t *po, const uint32_t *pp, uint32_t np,
+                      uint32_t *Sp, uint32_t &nc, cudaStream_t st) {
+    auto kern = k_seq_step_mma<VT, KPV, KP>;
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SMMA_WARPS * 32, 0);
+        occ = std::max(1, std::min<int>(occ, (int)MAX_STEP_CTAS_PER_SM));
+    }
+    const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    const uint32_t nctas = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)num_sms() * occ, (items + SMMA_WARPS - 1) / SMMA_WARPS));
+    kern<<<nctas, SMMA_WARPS * 32, 0, st>>>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp);
+    count_launch();
+    nc = nctas;
+    return (int)cudaGetLastError();
+}
+
+template <class VT>
+int launch_step_mma(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku, const uint16_t *Vin,
+                    uint16_t *Vout, const uint32_t *U, const uint32_t *ufrag, uint32_t *po,
+                    const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc, cudaStream_t st) {
+    if (k <= 4) return launch_step_mma_t<VT, 1, 4>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+    if (k <= 8) return launch_step_mma_t<VT, 2, 8>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+    return launch_step_mma_t<VT, 4, 16>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+}
+
+int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X, uint32_t ku,
+                     const uint32_t *U, uint64_t L, uint32_t *S, uint32_t *V_out,
+                     const SeqLayout<uint16_t> &W, uint32_t nctas, cudaStream_t st) {
+    const uint64_t n = op.rows;
+    const uint32_t *Uu = U ? U : X;
+    const uint32_t pairs = ku * k;
+    int err;
+    {
+        uint64_t tot = n * (uint64_t)k;
+        uint32_t blocks = (uint32_t)std::min<uint64_t>((tot + 255) / 256, (uint64_t)num_sms() * 8);
+        k_seq_prep<uint16_t><<<std::max<uint32_t>(blocks, 1), 256, 0, st>>>(X, Uu, tot, 0, W.V[0], W.Uc);
+        count_launch();
+        if (op.n_slices) {
+            uint64_t words = (uint64_t)op.n_slices * 256;
+            uint32_t fblocks = (uint32_t)std::min<uint64_t>((words + 255) / 256, (uint64_t)num_sms() * 8);
+            k_seq_ufrag<<<fblocks, 256, 0, st>>>(Uu, ku, op.perm, op.slices, op.n_slices, W.ufrag);
+            count_launch();
+        }
+    }
+    // S_0 partials straight from the caller's u32 X and U
+    if ((err = project<uint32_t>(X, Uu, ku, M, n, k, ku, W.partial[0], nctas, nullptr, st)))
+        return err;
+    uint32_t nprev = nctas;
+    for (uint64_t t = 1; t < L; ++t) {
+        uint32_t nc = 0;
+        const uint16_t *Vin = W.V[(t - 1) & 1];
+        uint16_t *Vout = W.V[t & 1];
+        uint32_t *po = W.partial[t & 1];
+        const uint32_t *pp = W.partial[(t - 1) & 1];
+        uint32_t *Sp = S + (t - 1) * pairs;
+        err = M.vbytes == 1
+                  ? launch_step_mma<uint8_t>(op, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st)
+                  : launch_step_mma<uint16_t>(op, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
+        if (err) return err;
+        nprev = nc;
+    }
+    k_seq_finalize<<<(pairs + 7) / 8, 256, 0, st>>>(W.partial[(L - 1) & 1], nprev, pairs, M,
+                                                   S + (L - 1) * pairs);
+    count_launch();
+    if (V_out) {
+        if ((err = launch_block_t<uint16_t, uint32_t>(op, M, k, 1u, W.V[(L - 1) & 1], k, 0u, V_out,
+                                                      k, (void *)st)))
+            return err;
+    }
+    return (int)cudaGetLastError();
+}
+
 template <class IT>
 int run_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X, uint32_t ku,
                  const uint32_t *U, uint64_t L, uint32_t *S, uint32_t *V_out, void *ws,
                  cudaStream_t st) {
     const uint64_t n = op.rows;
     const uint32_t nctas = proj_ctas(n);
-    SeqLayout<IT> W = layout<IT>(ws, n, k, ku, nctas);
+    SeqLayout<IT> W = layout<IT>(ws, op, M.m, k, ku, nctas);
     if (L == 0) {
         if (V_out && n)
             return (int)cudaMemcpyAsync(V_out, X, n * (size_t)k * 4, cudaMemcpyDeviceToDevice, st);
         return 0;
+    }
+    if constexpr (sizeof(IT) == 2) {
+        if (mma_ok(M.m, k, ku)) return run_sequence_mma(op, M, k, X, ku, U, L, S, V_out, W, nctas, st);
     }
     const bool fused = fused_ok(k, ku);
     const uint32_t ldu = fused ? kup_for(ku) : ku;
@@ -382,8 +472,8 @@ int run_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X
 size_t sequence_workspace(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku) {
     const uint64_t n = op.rows;
     const uint32_t nctas = proj_ctas(n);
-    if (M.m <= 65536u) return layout<uint16_t>(nullptr, n, k, ku, nctas).bytes;
-    return layout<uint32_t>(nullptr, n, k, ku, nctas).bytes;
+    if (M.m <= 65536u) return layout<uint16_t>(nullptr, op, M.m, k, ku, nctas).bytes;
+    return layout<uint32_t>(nullptr, op, M.m, k, ku, nctas).bytes;
 }
 
 int launch_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X, uint32_t ku,

@@ -1,0 +1,318 @@
+// Fused sequence step with a tensor-core projection (SURVEY §8 a-8 + a-9).
+//
+// One persistent launch per step computes V_{t+1} = A V_t for the SELL
+// slices with 4-column vector gathers of the u16 iterate, and the projection
+// U^T V_{t+1} of each 32-row slice as a 16 x k x 32 integer contraction on the
+// tensor cores: residues < 2^16 are split into u8 limbs (hi, lo) and
+//   U^T V = 2^16 Uh^T Vh + 2^8 (Uh^T Vl + Ul^T Vh) + Ul^T Vl
+// with mma.sync.m16n8k32 u8 x u8 -> s32 (exact: a slice adds at most
+// 32 * 255^2 per element; the s32 accumulators are folded into u64 every 512
+// slices).  The projection is a real contraction (k_u * k * N MACs per step,
+// more than the SpMM's k * nnz) but too small for tcgen05's M >= 64 tiles
+// (M = k_u = 16), hence the warp-level MMA.
+//
+// U is constant over the sequence, so its limbs are pre-arranged once per call
+// in fragment order (U_frag: per slice 2 planes x 32 lanes x 16 bytes), and a
+// warp loads its A fragments with two coalesced 16-byte loads per slice.  The
+// warp writes the slice's fresh V values into a shared tile transposed by
+// column (VT[plane][col][row], bytes), from which the B fragments are read.
+//
+// Rows outside SELL slices (long rows, CSR / COO_S groups, zero rows) take the
+// scalar path and add their projection with shared-memory atomics.
+#pragma once
+
+#include "block.cuh"
+
+namespace ffspmv {
+
+constexpr int SMMA_WARPS = 8;
+constexpr int SMMA_KMAX = 16;     // iterate columns handled by the fused kernel (k <= 16)
+constexpr int SMMA_FOLD = 512;    // slices between s32 -> u64 folds
+
+// NR consecutive rows x 4 columns per lane: KPV = k/4 lanes per row (1, 2,
+// 4), G = 32/KPV row groups, group g owns rows NR*g .. NR*g+NR-1, so a lane's
+// values of one column pack into NR bytes of the transposed tile.
+template <int KPV>
+struct SeqShape {
+    static constexpr int G = 32 / KPV;   // row groups
+    static constexpr int NR = 32 / G;    // rows per lane (= KPV)
+    static_assert(NR <= 4, "fused MMA path: k <= 16");
+};
+
+__device__ __forceinline__ void mma_u8(int (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// U fragment layout for slice s (ku <= 16): plane q (0 = hi, 1 = lo), lane,
+// register j: bytes b = 0..3 hold U_q[row r][col a] with
+//   a = (lane >> 2) + 8 * (j & 1),  r = (lane & 3) * 4 + 16 * (j >> 1) + b
+// (the m16n8k32 A-operand layout, A[a][r] = U[r][a]).
+__global__ void k_seq_ufrag(const uint32_t *__restrict__ U, uint32_t ku, const uint32_t *__restrict__ perm,
+                            const SliceHdr *__restrict__ slices, uint32_t nslices,
+                            uint32_t *__restrict__ ufrag) {
+    const uint64_t total = (uint64_t)nslices * 2 * 32 * 4;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = i & 3, lane = (i >> 2) & 31, q = (i >> 7) & 1;
+        const uint64_t s = i >> 8;
+        const uint32_t a = (lane >> 2) + 8 * (j & 1);
+        const uint32_t nrows = slices[s].nrows;
+        uint32_t word = 0;
+        for (uint32_t b = 0; b < 4; ++b) {
+            const uint32_t r = (lane & 3) * 4 + 16 * (j >> 1) + b;
+            uint32_t v = 0;
+            if (r < nrows && a < ku) {
+                const uint32_t row = perm[s * 32 + r];
+                const uint32_t u = U[(uint64_t)row * ku + a];
+                v = q == 0 ? (u >> 8) & 0xFFu : u & 0xFFu;
+            }
+            word |= v << (8 * b);
+        }
+        ufrag[i] = word;
+    }
+}
+
+struct SmmaState {
+    int acc[4][SMMA_KMAX / 8][4];       // [limb combo][n-tile][frag]: hh, hl, lh, ll
+    unsigned long long p64[SMMA_KMAX / 8][4];
+    uint32_t since_fold;
+};
+
+__device__ __forceinline__ void smma_fold(SmmaState &st, int nt_count) {
+#pragma unroll
+    for (int nt = 0; nt < SMMA_KMAX / 8; ++nt) {
+        if (nt >= nt_count) break;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            st.p64[nt][e] += ((unsigned long long)(uint32_t)st.acc[0][nt][e] << 16) +
+                             (((unsigned long long)(uint32_t)st.acc[1][nt][e] +
+                               (uint32_t)st.acc[2][nt][e]) << 8) +
+                             (uint32_t)st.acc[3][nt][e];
+            st.acc[0][nt][e] = st.acc[1][nt][e] = st.acc[2][nt][e] = st.acc[3][nt][e] = 0;
+        }
+    }
+    st.since_fold = 0;
+}
+
+// SpMM of one SELL slice (u16 iterate, 4 columns per lane) + its projection.
+template <class Acc, class VT, int KPV>
+__device__ __forceinline__ void seq_slice_mma(const DevOp &op, const DevMod &M, uint32_t s,
+                                              const SliceHdr &h, uint32_t lane, uint32_t k,
+                                              const uint16_t *__restrict__ Vin,
+                                              uint16_t *__restrict__ Vout,
+                                              const uint32_t *__restrict__ ufrag,
+                                              uint8_t *vt, SmmaState &st) {
+    using S = SeqShape<KPV>;
+    const uint32_t g = lane / KPV, cl = lane % KPV;
+    const uint32_t col = cl * 4;
+    const bool colok = col < k;
+    const uint32_t m = M.m;
+    const uint32_t *pc = op.pcol + h.off_p + lane;
+    const uint32_t *vc = op.vcol + h.off_v + lane;
+    const VT *vv = reinterpret_cast<const VT *>(op.vval) + h.off_v + lane;
+    const uint32_t wp = h.wp, wv = h.wv;
+    const uint32_t rbase = g * S::NR;
+    Acc acc[S::NR][4];
+    uint32_t cw = wp ? ld_bcast(pc) : PAD_COL;
+    for (uint32_t j = 0; j < wp; ++j) {
+        const uint32_t cur = cw;
+        if (j + 1 < wp) cw = ld_bcast(pc + (j + 1) * 32);
+        uint32_t xv[S::NR][4], cs[S::NR];
+#pragma unroll
+        for (int i = 0; i < S::NR; ++i) {
+            cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i);
+            if (cs[i] != PAD_COL && colok) {
+                ld_vec<uint16_t, 4>(Vin + ((cs[i] & COL_MASK) * k + col), xv[i]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) xv[i][c] = 0;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < S::NR; ++i)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[i][c].add((cs[i] & SIGN_BIT) ? m - xv[i][c] : xv[i][c]);
+    }
+    uint32_t vw = wv ? ld_bcast(vc) : PAD_COL;
+    uint32_t aw = wv ? ld_bcast(vv) : 0u;
+    for (uint32_t j = 0; j < wv; ++j) {
+        const uint32_t cur = vw, cura = aw;
+        if (j + 1 < wv) { vw = ld_bcast(vc + (j + 1) * 32); aw = ld_bcast(vv + (j + 1) * 32); }
+        uint32_t xv[S::NR][4], as[S::NR];
+#pragma unroll
+        for (int i = 0; i < S::NR; ++i) {
+            const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i);
+            as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i);
+            if (c != PAD_COL && colok) {
+                ld_vec<uint16_t, 4>(Vin + (c * k + col), xv[i]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) xv[i][q] = 0;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < S::NR; ++i)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[i][c].mad(as[i], xv[i][c]);
+    }
+    // residues -> V_{t+1} (8-byte stores) and the transposed limb tile
+    uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < S::NR; ++i) {
+        const uint32_t r = rbase + i;
+        uint32_t v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = acc[i][c].reduce(M);
+        if (r < h.nrows && colok) {
+            const uint32_t row = op.perm[s * 32 + r];
+            uint2 w;
+            w.x = v[0] | (v[1] << 16);
+            w.y = v[2] | (v[3] << 16);
+            *reinterpret_cast<uint2 *>(Vout + (uint64_t)row * k + col) = w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = 0;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            hi[c] |= ((v[c] >> 8) & 0xFFu) << (8 * i);
+            lo[c] |= (v[c] & 0xFFu) << (8 * i);
+        }
+    }
+    // VT[plane][col][row]: 32 x 32 bytes per plane; this lane owns rows
+    // rbase .. rbase+NR-1 (NR bytes, NR-aligned) of columns col..col+3
+    if (colok) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint8_t *ph = vt + (col + c) * 32 + rbase, *pl = ph + 32 * 32;
+            if constexpr (S::NR == 4) {
+                *reinterpret_cast<uint32_t *>(ph) = hi[c];
+                *reinterpret_cast<uint32_t *>(pl) = lo[c];
+            } else if constexpr (S::NR == 2) {
+                *reinterpret_cast<uint16_t *>(ph) = (uint16_t)hi[c];
+                *reinterpret_cast<uint16_t *>(pl) = (uint16_t)lo[c];
+            } else {
+                *ph = (uint8_t)hi[c];
+                *pl = (uint8_t)lo[c];
+            }
+        }
+    }
+    __syncwarp();
+    // A fragments (U limbs) of this slice: two coalesced 16-byte loads
+    const uint4 ah4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256) + lane);
+    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
+    const uint32_t ah[4] = {ah4.x, ah4.y, ah4.z, ah4.w}, al[4] = {al4.x, al4.y, al4.z, al4.w};
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+    const int ntiles = (int)((k + 7) / 8);
+#pragma unroll
+    for (int nt = 0; nt < SMMA_KMAX / 8; ++nt) {
+        if (nt >= ntiles) break;
+        const uint32_t b = nt * 8 + gid;
+        uint32_t bh[2], bl[2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const uint32_t off = b * 32 + tig * 4 + 16 * jj;
+            bh[jj] = *reinterpret_cast<const uint32_t *>(vt + off);
+            bl[jj] = *reinterpret_cast<const uint32_t *>(vt + 32 * 32 + off);
+        }
+        mma_u8(st.acc[0][nt], ah, bh);
+        mma_u8(st.acc[1][nt], ah, bl);
+        mma_u8(st.acc[2][nt], al, bh);
+        mma_u8(st.acc[3][nt], al, bl);
+    }
+    __syncwarp();
+    if (++st.since_fold == SMMA_FOLD) smma_fold(st, ntiles);
+}
+
+// Output policy of the scalar path inside the fused kernel: V_{t+1} and the
+// projection through shared-memory u64 atomics (rare rows only).
+struct SeqScalarOut {
+    uint16_t *V;
+    const uint32_t *U;
+    uint32_t k, ku;
+    unsigned long long *pn;   // shared [ku][k]
+    __device__ __forceinline__ void put(uint32_t row, uint32_t col, bool colok, uint32_t r,
+                                        const DevMod &) {
+        if (!colok) return;
+        V[(uint64_t)row * k + col] = (uint16_t)r;
+        if (r == 0) return;
+        for (uint32_t a = 0; a < ku; ++a)
+            atomicAdd(pn + a * k + col, (unsigned long long)U[(uint64_t)row * ku + a] * r);
+    }
+};
+
+template <class VT, int KPV, int KP>
+__global__ void __launch_bounds__(SMMA_WARPS * 32)
+k_seq_step_mma(DevOp op, DevMod M, uint32_t k, uint32_t ku, const uint16_t *__restrict__ Vin,
+               uint16_t *__restrict__ Vout, const uint32_t *__restrict__ U,
+               const uint32_t *__restrict__ ufrag, uint32_t *__restrict__ part_out,
+               const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev) {
+    __shared__ __align__(16) uint8_t vts[SMMA_WARPS][2 * 32 * 32];
+    __shared__ unsigned long long pn[16 * SMMA_KMAX];
+    __shared__ uint32_t red[SMMA_WARPS][16][SMMA_KMAX];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
+    const uint32_t pairs = ku * k;
+    for (uint32_t i = threadIdx.x; i < 16 * SMMA_KMAX; i += SMMA_WARPS * 32) pn[i] = 0;
+    __syncthreads();
+    // finalise the previous step's S from its CTA partials
+    for (uint32_t p = gw; part_prev && p < pairs; p += nw) {
+        uint64_t s = 0;
+        for (uint32_t c = lane; c < nprev; c += 32) s += part_prev[(uint64_t)c * pairs + p];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        if (lane == 0) S_prev[p] = mod64(s, M);
+    }
+    SmmaState st;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int nt = 0; nt < SMMA_KMAX / 8; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) st.acc[c][nt][e] = 0;
+#pragma unroll
+    for (int nt = 0; nt < SMMA_KMAX / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) st.p64[nt][e] = 0;
+    st.since_fold = 0;
+    SeqScalarOut sout{Vout, U, k, ku, pn};
+    const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    for (uint32_t w = gw; w < items; w += nw) {
+        if (w >= op.n_long && w - op.n_long < op.n_slices) {
+            const uint32_t s = w - op.n_long;
+            const SliceHdr h = load_hdr_b(op.slices + s);
+            switch (h.regime) {
+                case ACC32: seq_slice_mma<Acc32, VT, KPV>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], st); break;
+                default: seq_slice_mma<Acc64, VT, KPV>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], st); break;
+            }
+        } else {
+            block_item<VT, KP, 8>(op, M, w, lane, k, Vin, k, sout);
+        }
+    }
+    const int ntiles = (int)((k + 7) / 8);
+    smma_fold(st, ntiles);
+    // C fragment: element e of n-tile nt is (a = gid + 8*(e>>1), b = nt*8 + tig*2 + (e&1))
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < SMMA_KMAX / 8; ++nt) {
+        if (nt >= ntiles) break;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t a = gid + 8 * (e >> 1), b = nt * 8 + tig * 2 + (e & 1);
+            red[warp][a][b] = mod64(st.p64[nt][e], M);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < pairs; i += SMMA_WARPS * 32) {
+        const uint32_t a = i / k, b = i - a * k;
+        uint64_t s = mod64(pn[a * k + b], M);
+#pragma unroll
+        for (int w = 0; w < SMMA_WARPS; ++w) s += red[w][a][b];
+        part_out[(uint64_t)blockIdx.x * pairs + i] = mod64(s, M);
+    }
+}
+
+}  // namespace ffspmv
