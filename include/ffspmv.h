@@ -86,7 +86,8 @@ enum {
 enum { FFSPMV_STRATEGY_AUTO = 0, FFSPMV_STRATEGY_ROWS = 1, FFSPMV_STRATEGY_PANELS = 2 };
 
 /* Operation selectors for ffspmv_apply_host / ffspmv_workspace_size. */
-enum { FFSPMV_OP_APPLY = 0, FFSPMV_OP_TRANSPOSE = 1, FFSPMV_OP_BLOCK = 2, FFSPMV_OP_SEQUENCE = 3 };
+enum { FFSPMV_OP_APPLY = 0, FFSPMV_OP_TRANSPOSE = 1, FFSPMV_OP_BLOCK = 2, FFSPMV_OP_SEQUENCE = 3,
+       FFSPMV_OP_PROJECT = 4 };
 
 /* Creation options.  A zero-initialised struct (with struct_size set) means
  * "all defaults". */
@@ -238,6 +239,21 @@ FFSPMV_API ffspmv_status ffspmv_sequence(ffspmv_matrix A, uint32_t k, const uint
                                          uint32_t ku, const uint32_t *U, uint64_t L,
                                          uint32_t *S, uint32_t *V_out, void *workspace,
                                          size_t workspace_bytes, void *stream);
+
+/* Projection of one block (the "dense dot products by U^T" of P:459-460):
+ *   S[a][b] = sum_r U[r][a] * V[r][b] mod m,  r < rows(A),
+ * V: rows(A) x k, U: rows(A) x ku (device, row-major), S: ku x k (device).
+ * Used by the row-banded multi-GPU sequence, where A is a rank's band and V,
+ * U its rows.  workspace >= ffspmv_workspace_size(A, FFSPMV_OP_PROJECT, k, ku).
+ * Errors: INVALID_ARG, NOMEM (workspace), CUDA. */
+FFSPMV_API ffspmv_status ffspmv_project(ffspmv_matrix A, uint32_t k, const uint32_t *V,
+                                        uint32_t ku, const uint32_t *U, uint32_t *S,
+                                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* out[i] = sum_p parts[p * count + i] mod m, for combining per-rank residues
+ * (e.g. the band projections after an all-gather).  Device pointers. */
+FFSPMV_API ffspmv_status ffspmv_sum_mod(ffspmv_matrix A, uint64_t count, uint32_t nparts,
+                                        const uint32_t *parts, uint32_t *out, void *stream);
 
 /* --- diagnostics ------------------------------------------------------------ */
 

@@ -22,14 +22,14 @@ OK, ERR_INVALID_ARG, ERR_MODULUS, ERR_INDEX, ERR_DIM, ERR_NONSQUARE, ERR_UNSUPPO
     ERR_NOMEM, ERR_CUDA, ERR_NCCL = range(10)
 FMT_AUTO, FMT_SELL, FMT_CSR, FMT_COOS = range(4)
 STRATEGY_AUTO, STRATEGY_ROWS, STRATEGY_PANELS = range(3)
-OP_APPLY, OP_TRANSPOSE, OP_BLOCK, OP_SEQUENCE = range(4)
+OP_APPLY, OP_TRANSPOSE, OP_BLOCK, OP_SEQUENCE, OP_PROJECT = range(5)
 
 # Every symbol include/ffspmv.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "ffspmv_create", "ffspmv_destroy", "ffspmv_get_info", "ffspmv_analyze", "ffspmv_apply",
     "ffspmv_apply_transpose", "ffspmv_apply_block", "ffspmv_apply_host",
-    "ffspmv_workspace_size", "ffspmv_sequence", "ffspmv_status_string", "ffspmv_last_error",
-    "ffspmv_version", "ffspmv_kernel_launches",
+    "ffspmv_workspace_size", "ffspmv_sequence", "ffspmv_project", "ffspmv_sum_mod",
+    "ffspmv_status_string", "ffspmv_last_error", "ffspmv_version", "ffspmv_kernel_launches",
 ]
 
 
@@ -121,6 +121,8 @@ def load(path: str = LIB_PATH):
         "ffspmv_apply_host": [P, i32, u32, P, u32, P, P],
         "ffspmv_workspace_size": [P, i32, u32, u32, ctypes.POINTER(ctypes.c_size_t)],
         "ffspmv_sequence": [P, u32, P, u32, P, u64, P, P, P, ctypes.c_size_t, P],
+        "ffspmv_project": [P, u32, P, u32, P, P, P, ctypes.c_size_t, P],
+        "ffspmv_sum_mod": [P, u64, u32, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -367,3 +369,18 @@ def ffspmv_sequence(A, k, X, ku, U, L, S, V_out, workspace, stream=None):
     _check(load().ffspmv_sequence(_h(A), k, _ptr(X), ku, _ptr(U), L, _ptr(S), _ptr(V_out), ws,
                                   nbytes, _stream(stream)))
     return S
+
+
+def ffspmv_project(A, k, V, ku, U, S, workspace, stream=None):
+    """S = U^T V mod m over the rows of A (ku x k)."""
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else None
+    _check(load().ffspmv_project(_h(A), k, _ptr(V), ku, _ptr(U), _ptr(S), ws, nbytes,
+                                 _stream(stream)))
+    return S
+
+
+def ffspmv_sum_mod(A, count, nparts, parts, out, stream=None):
+    """out[i] = sum_p parts[p*count + i] mod m (device tensors)."""
+    _check(load().ffspmv_sum_mod(_h(A), count, nparts, _ptr(parts), _ptr(out), _stream(stream)))
+    return out

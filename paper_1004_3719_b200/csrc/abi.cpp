@@ -579,6 +579,12 @@ ffspmv_status ffspmv_apply_host(ffspmv_matrix A, int which, uint32_t alpha, cons
 ffspmv_status ffspmv_workspace_size(ffspmv_matrix A, int which, uint32_t k, uint32_t ku,
                                     size_t *bytes) {
     if (!A || !bytes) return fail(FFSPMV_ERR_INVALID_ARG, "NULL argument");
+    if (which == FFSPMV_OP_PROJECT) {
+        if (k == 0 || ku == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k and ku must be >= 1");
+        DeviceGuard guard(A->device);
+        *bytes = project_workspace(A->has_op[0] ? A->op[0].rows : A->pan[0].rows, k, ku);
+        return FFSPMV_OK;
+    }
     if (which != FFSPMV_OP_SEQUENCE) { *bytes = 0; return FFSPMV_OK; }
     if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
     if (ku == 0) ku = k;
@@ -625,6 +631,39 @@ ffspmv_status ffspmv_sequence(ffspmv_matrix A, uint32_t k, const uint32_t *X, ui
     }
     int e = launch_sequence(op, A->mod, k, X, ku, U, L, S, V_out, workspace, workspace_bytes, stream);
     if (e) return cuda_fail(e, "sequence launch");
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_project(ffspmv_matrix A, uint32_t k, const uint32_t *V, uint32_t ku,
+                             const uint32_t *U, uint32_t *S, void *workspace,
+                             size_t workspace_bytes, void *stream) {
+    if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (k == 0 || ku == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k and ku must be >= 1");
+    const uint64_t n = A->has_op[0] ? A->op[0].rows : A->pan[0].rows;
+    if ((n && (!V || !U)) || !S) return fail(FFSPMV_ERR_INVALID_ARG, "NULL V, U or S");
+    if (overlaps(S, (size_t)ku * k * 4, V, n * k * 4) || overlaps(S, (size_t)ku * k * 4, U, n * ku * 4))
+        return fail(FFSPMV_ERR_INVALID_ARG, "S overlaps an input");
+    DeviceGuard guard(A->device);
+    const size_t need = project_workspace(n, k, ku);
+    if (n && (!workspace || workspace_bytes < need))
+        return fail(FFSPMV_ERR_NOMEM, "workspace smaller than ffspmv_workspace_size (" +
+                                          std::to_string(need) + " bytes)");
+    ffspmv_status s;
+    if ((s = check_vec(A, V, n, k, k, stream, "V"))) return s;
+    if ((s = check_vec(A, U, n, ku, ku, stream, "U"))) return s;
+    int e = launch_project(A->mod, n, k, V, ku, U, S, workspace, stream);
+    if (e) return cuda_fail(e, "project launch");
+    return FFSPMV_OK;
+}
+
+ffspmv_status ffspmv_sum_mod(ffspmv_matrix A, uint64_t count, uint32_t nparts,
+                             const uint32_t *parts, uint32_t *out, void *stream) {
+    if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (count && (!parts || !out || nparts == 0))
+        return fail(FFSPMV_ERR_INVALID_ARG, "NULL parts/out or nparts == 0");
+    DeviceGuard guard(A->device);
+    int e = launch_sum_mod(A->mod, count, nparts, parts, out, stream);
+    if (e) return cuda_fail(e, "sum_mod launch");
     return FFSPMV_OK;
 }
 

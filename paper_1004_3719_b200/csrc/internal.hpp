@@ -204,6 +204,11 @@ int launch_block(const DevOp &op, const DevMod &M, uint32_t k, uint32_t alpha,
                  const uint32_t *X, uint64_t ldx, uint32_t beta, uint32_t *Y, uint64_t ldy,
                  void *stream);
 size_t sequence_workspace(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku);
+size_t project_workspace(uint64_t n, uint32_t k, uint32_t ku);
+int launch_project(const DevMod &M, uint64_t n, uint32_t k, const uint32_t *V, uint32_t ku,
+                   const uint32_t *U, uint32_t *S, void *ws, void *stream);
+int launch_sum_mod(const DevMod &M, uint64_t count, uint32_t nparts, const uint32_t *parts,
+                   uint32_t *out, void *stream);
 int launch_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X,
                     uint32_t ku, const uint32_t *U, uint64_t L, uint32_t *S, uint32_t *V_out,
                     void *ws, size_t ws_bytes, void *stream);

@@ -469,6 +469,38 @@ int run_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X
 
 }  // namespace
 
+// Stand-alone projection S = U^T V mod m (ku x k) of an n-row block, for the
+// row-banded multi-GPU sequence (each rank projects its band).
+size_t project_workspace(uint64_t n, uint32_t k, uint32_t ku) {
+    return align256((size_t)proj_ctas(n) * ku * k * sizeof(uint32_t));
+}
+
+int launch_project(const DevMod &M, uint64_t n, uint32_t k, const uint32_t *V, uint32_t ku,
+                   const uint32_t *U, uint32_t *S, void *ws, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) return (int)cudaMemsetAsync(S, 0, (size_t)ku * k * 4, st);
+    return project<uint32_t>(V, U, ku, M, n, k, ku, (uint32_t *)ws, proj_ctas(n), S, st);
+}
+
+__global__ void k_sum_mod(const uint32_t *__restrict__ parts, uint64_t count, uint32_t nparts,
+                          DevMod M, uint32_t *__restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t s = 0;   // nparts residues < 2^32 each: exact for nparts < 2^32
+        for (uint32_t p = 0; p < nparts; ++p) s += parts[(uint64_t)p * count + i];
+        out[i] = mod64(s, M);
+    }
+}
+
+int launch_sum_mod(const DevMod &M, uint64_t count, uint32_t nparts, const uint32_t *parts,
+                   uint32_t *out, void *stream) {
+    if (count == 0) return 0;
+    uint32_t blocks = (uint32_t)std::min<uint64_t>((count + 255) / 256, (uint64_t)num_sms() * 8);
+    k_sum_mod<<<blocks, 256, 0, (cudaStream_t)stream>>>(parts, count, nparts, M, out);
+    count_launch();
+    return (int)cudaGetLastError();
+}
+
 size_t sequence_workspace(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku) {
     const uint64_t n = op.rows;
     const uint32_t nctas = proj_ctas(n);

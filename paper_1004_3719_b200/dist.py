@@ -2,24 +2,25 @@
 the plumbing (NCCL over NVLink on the GPU box; gloo in the CPU tests).
 
 The partitioning is host logic; every product runs in the C ABI kernels of
-the calling rank.  Two modes of the block Wiedemann sequence:
+the calling rank (``CudaBackend``).  Two modes of the block Wiedemann sequence
+(P:457-463):
 
-* ``sequence_columns``  -- the paper's "ship independent set of vector blocks
+* ``sequence_columns`` -- the paper's "ship independent set of vector blocks
   of V to different cores ... then gather the results": rank r
   owns columns [c_r, c_{r+1}) of X, iterates them with its own copy of A and
   no per-step communication; the S column blocks are all-gathered once.
-* ``sequence_rows``     -- "let the SpMV library take care of the iteration"
-   across GPUs: rank r owns the rows [r_r, r_{r+1}) of A
+* ``sequence_rows``    -- "let the SpMV library take care of the iteration"
+   across GPUs: rank r owns the rows [b_r, b_{r+1}) of A
   (nnz-balanced bands); each step computes its band of V_{t+1} = A V_t,
-  all-gathers the bands into the full iterate, and accumulates its band's
-  projection U_band^T V_band; the L projections are summed over ranks once.
+  all-gathers the bands into the full iterate (the per-step exchange over
+  NVLink), and projects its band; the L band projections are combined once.
 
 Single applies shard by rows with no exchange (``row_bands``).  Every result
 is identical to the 1-GPU result (R20).
 
-``backend`` objects supply the per-rank compute, so the same host logic runs
-on the CUDA path (``CudaBackend``) and, in the CPU tests, on any exact
-reference implementation.
+The backend supplies the per-rank compute.  ``CudaBackend`` is the product
+path; the CPU tests substitute an exact reference backend to check the host
+logic (partitioning, gathers, assembly) under gloo with world_size 2.
 """
 from __future__ import annotations
 
@@ -35,11 +36,9 @@ def row_bands(row_idx, rows: int, world: int) -> np.ndarray:
     total = cum[-1]
     b = [0]
     for r in range(1, world):
-        target = total * r / world
-        b.append(int(np.searchsorted(cum, target, side="left")))
+        b.append(int(np.searchsorted(cum, total * r / world, side="left")))
     b.append(rows)
-    b = np.maximum.accumulate(np.clip(np.array(b, dtype=np.int64), 0, rows))
-    return b
+    return np.maximum.accumulate(np.clip(np.array(b, dtype=np.int64), 0, rows))
 
 
 def column_shards(k: int, world: int) -> np.ndarray:
@@ -86,17 +85,24 @@ class CudaBackend:
         import paper_1004_3719_b200 as ff
         return ff.ffspmv_apply_block(A, X.shape[1], 1, X, 0, out)
 
-    def project(self, A, V, U, m):
-        """S = U^T V mod m for one band: a length-1 sequence on the band's
-        iterate (identity product not needed: S_0 = U^T V)."""
-        raise NotImplementedError
+    def project(self, A, V, U, out):
+        import paper_1004_3719_b200 as ff
+        k, ku = V.shape[1], U.shape[1]
+        ws = self.torch.empty(max(1, ff.ffspmv_workspace_size(A, ff.OP_PROJECT, k, ku)),
+                              dtype=self.torch.uint8, device=self.device)
+        return ff.ffspmv_project(A, k, V, ku, U, out, ws)
+
+    def sum_mod(self, A, parts, out):
+        import paper_1004_3719_b200 as ff
+        return ff.ffspmv_sum_mod(A, out.numel(), parts.shape[0], parts, out)
 
 
-def _all_gather_rows(group, band_tensor, counts, torch):
+def _all_gather_rows(group, band_tensor, counts):
     """All-gather row bands of different heights (padded to the max height)."""
+    import torch
     import torch.distributed as dist
     world = len(counts)
-    hmax = int(max(counts))
+    hmax = max(1, int(max(counts)))
     k = band_tensor.shape[1]
     pad = torch.zeros((hmax, k), dtype=band_tensor.dtype, device=band_tensor.device)
     pad[: band_tensor.shape[0]] = band_tensor
@@ -121,20 +127,14 @@ def sequence_columns(n, row_idx, col_idx, vals, m, X, L, U, backend, group=None)
     c = column_shards(k, world)
     A = backend.create(n, n, row_idx, col_idx, vals, m)
     lo, hi = int(c[rank]), int(c[rank + 1])
-    if hi > lo:
-        S_loc = backend.to_numpy(backend.sequence(A, backend.tensor(X[:, lo:hi]), L,
-                                                  backend.tensor(U))).reshape(L, ku, hi - lo)
-    else:
-        S_loc = np.zeros((L, ku, 0), np.uint32)
-    # gather the column blocks (padded to the widest block)
-    wmax = int(max(c[1:] - c[:-1]))
-    buf = np.zeros((L, ku, wmax), np.uint32)
-    buf[:, :, : hi - lo] = S_loc
-    t = torch.from_numpy(buf.view(np.int32).copy())
+    wmax = max(1, int(max(c[1:] - c[:-1])))
     dev = getattr(backend, "device", torch.device("cpu"))
-    t = t.to(dev)
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t, group=group)
+    buf = torch.zeros((L, ku, wmax), dtype=torch.int32, device=dev)
+    if hi > lo and L:
+        S_loc = backend.sequence(A, backend.tensor(X[:, lo:hi]), L, backend.tensor(U))
+        buf[:, :, : hi - lo] = S_loc.reshape(L, ku, hi - lo)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
     S = np.zeros((L, ku, k), np.uint32)
     for r in range(world):
         w = int(c[r + 1] - c[r])
@@ -158,21 +158,20 @@ def sequence_rows(n, row_idx, col_idx, vals, m, X, L, U, backend, group=None, wa
     lo, hi = int(b[rank]), int(b[rank + 1])
     ri, ci, v = band_triples(row_idx, col_idx, vals, lo, hi)
     A_band = backend.create(hi - lo, n, ri, ci, v, m)
-    V = backend.tensor(X)                       # full iterate, replicated
-    U_band = U[lo:hi].astype(np.uint64)
-    S_part = np.zeros((L, ku, k), np.uint64)    # this band's projections (exact, < n * m^2)
+    V = backend.tensor(X)                               # full iterate, replicated
+    U_band = backend.tensor(U[lo:hi])
+    S_band = backend.empty((L, ku, k))                  # this band's projections (residues)
     for t in range(L):
-        Vb = backend.to_numpy(V)[lo:hi].astype(np.uint64)
-        # projection of this band, exact then reduced (object-free: per column)
-        S_part[t] = ((U_band.T.astype(object) @ Vb.astype(object)) % m).astype(np.uint64)
+        backend.project(A_band, V[lo:hi], U_band, S_band[t])
         if t + 1 < L or want_vout:
             out = backend.empty((hi - lo, k))
             backend.apply_block(A_band, V, out)
-            V = _all_gather_rows(group, out, counts, torch)
-    # sum the band projections over ranks (each < m, world * m < 2^63)
-    tot = torch.from_numpy(S_part.astype(np.int64))
-    dist.all_reduce(tot, group=group)
-    S = (tot.numpy() % m).astype(np.uint32)
+            V = _all_gather_rows(group, out, counts)    # the per-step exchange
+    parts = [torch.empty_like(S_band) for _ in range(world)]
+    dist.all_gather(parts, S_band, group=group)
+    S = backend.empty((L, ku, k))
+    backend.sum_mod(A_band, torch.stack(parts), S)      # sum_r S_r mod m on device
+    S = backend.to_numpy(S)
     if want_vout:
         return S, backend.to_numpy(V)
     return S
