@@ -24,7 +24,29 @@ namespace {
 
 constexpr int PANEL_THREADS = 1024;
 constexpr int PBP = 4;  // +-1 entries per thread per round (all loads issued first)
-constexpr int PBV = 6;  // valued entries per thread per round
+constexpr int PBV = 8;  // valued entries per thread per round
+
+// Shared-memory accesses through 32-bit shared addresses (no generic-address
+// conversion in the hot loop).
+template <class IT>
+__device__ __forceinline__ uint32_t lds_x(uint32_t base, uint32_t i) {
+    uint32_t v;
+    if constexpr (sizeof(IT) == 1) {
+        unsigned short h;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=h"(h) : "r"(base + i));
+        v = h;
+    } else if constexpr (sizeof(IT) == 2) {
+        unsigned short h;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + 2 * i));
+        v = h;
+    } else {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + 4 * i));
+    }
+    return v;
+}
+
+template <bool SPLIT>
+__device__ __forceinline__ void acc_add_s(uint32_t acc_s, uint32_t row, uint32_t v);
 constexpr uint32_t PANEL_NONE = 0xFFFFFFFFu;  // no entry (bit 31 of a packed word is 0)
 
 template <bool SPLIT>
@@ -55,6 +77,16 @@ __device__ __forceinline__ void acc_add(uint32_t *acc, uint32_t row, uint32_t v)
         atomicAdd(acc + ACC_STRIDE + row, v >> 16);
     } else {
         atomicAdd(acc + row, v);
+    }
+}
+
+template <bool SPLIT>
+__device__ __forceinline__ void acc_add_s(uint32_t acc_s, uint32_t row, uint32_t v) {
+    if constexpr (SPLIT) {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(acc_s + 4 * row), "r"(v & 0xFFFFu));
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(acc_s + 4 * (ACC_STRIDE + row)), "r"(v >> 16));
+    } else {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(acc_s + 4 * row), "r"(v));
     }
 }
 
@@ -129,6 +161,8 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
     const PanelGeom g = op.g;
     IT *sx = reinterpret_cast<IT *>(smem);
     uint32_t *acc = reinterpret_cast<uint32_t *>(smem + (size_t)g.W * sizeof(IT));
+    const uint32_t sx_s = (uint32_t)__cvta_generic_to_shared(sx);
+    const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);
     const uint32_t t0 = op.cta_t0[blockIdx.x], t1 = op.cta_t0[blockIdx.x + 1];
     const VT *vval = reinterpret_cast<const VT *>(op.vval);
     for (uint32_t i = threadIdx.x; i < ACC_STRIDE * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
@@ -142,48 +176,55 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
             cur_p = p;
         }
         __syncthreads();
-        // the tile's +-1 and valued entries as one index space [0, np + nv):
-        // each round issues all PB loads of a thread before any shared op
-        // Masked-off lanes read a per-lane dummy word (row PANEL_DUMMY_ROW +
-        // lane, value 0) so the steady state has no branch.
-        // The +-1 part [0, np) and the valued part [np, n) advance together
-        // with their own specialised code; each round issues all loads of both
-        // before the first shared op (one memory round trip per round).
+        // The +-1 part [0, np) and the valued part [np, n) of the tile run as
+        // two specialised loops; every round issues all its loads before the
+        // first shared op, and the first valued round is loaded before the
+        // +-1 loop so the two streams share one memory round trip.
         {
             const uint32_t e0 = op.tp[t], n = op.tp[t + 1] - e0;
             const uint32_t v0 = op.tv[t], nv = op.tv[t + 1] - v0, np = n - nv;
             const uint32_t *pw = op.pent + e0, *vw = op.pent + e0 + np;
             const VT *va = vval + v0;
-            const uint32_t rounds = max((np + PBP * PANEL_THREADS - 1) / (PBP * PANEL_THREADS),
-                                        (nv + PBV * PANEL_THREADS - 1) / (PBV * PANEL_THREADS));
             const uint32_t m = M.m;
-            for (uint32_t rd = 0; rd < rounds; ++rd) {
-                uint32_t w[PBP], x[PBV], a[PBV];
+            uint32_t x[PBV], a[PBV];
+#pragma unroll
+            for (int u = 0; u < PBV; ++u) {
+                const uint32_t e = u * PANEL_THREADS + threadIdx.x;
+                x[u] = e < nv ? ld_stream(vw + e) : PANEL_NONE;
+                a[u] = e < nv ? ld_stream(va + e) : 0u;
+            }
+            for (uint32_t base = threadIdx.x; base < np; base += PBP * PANEL_THREADS) {
+                uint32_t w[PBP];
 #pragma unroll
                 for (int u = 0; u < PBP; ++u) {
-                    const uint32_t e = (rd * PBP + u) * PANEL_THREADS + threadIdx.x;
+                    const uint32_t e = base + u * PANEL_THREADS;
                     w[u] = e < np ? ld_stream(pw + e) : PANEL_NONE;
-                }
-#pragma unroll
-                for (int u = 0; u < PBV; ++u) {
-                    const uint32_t e = (rd * PBV + u) * PANEL_THREADS + threadIdx.x;
-                    x[u] = e < nv ? ld_stream(vw + e) : PANEL_NONE;
-                    a[u] = e < nv ? ld_stream(va + e) : 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < PBP; ++u) {
                     if (w[u] != PANEL_NONE) {
-                        const uint32_t xv = sx[w[u] & 0xFFFFu];
+                        const uint32_t xv = lds_x<IT>(sx_s, w[u] & 0xFFFFu);
                         const uint32_t ad = (w[u] & PANEL_SIGN) ? (xv ? m - xv : 0u) : xv;
-                        acc_add<SPLIT>(acc, w[u] >> PANEL_ROW_SHIFT, ad);
+                        acc_add_s<SPLIT>(acc_s, w[u] >> PANEL_ROW_SHIFT, ad);
                     }
                 }
+            }
+            for (uint32_t base = threadIdx.x;; ) {
 #pragma unroll
                 for (int u = 0; u < PBV; ++u) {
                     if (x[u] != PANEL_NONE) {
-                        const uint32_t xv = sx[x[u] & 0xFFFFu];
-                        acc_add<SPLIT>(acc, x[u] >> PANEL_ROW_SHIFT, addend<SPLIT>(true, 0, a[u], xv, M));
+                        const uint32_t xv = lds_x<IT>(sx_s, x[u] & 0xFFFFu);
+                        acc_add_s<SPLIT>(acc_s, x[u] >> PANEL_ROW_SHIFT,
+                                         addend<SPLIT>(true, 0, a[u], xv, M));
                     }
+                }
+                base += PBV * PANEL_THREADS;
+                if (base >= nv) break;
+#pragma unroll
+                for (int u = 0; u < PBV; ++u) {
+                    const uint32_t e = base + u * PANEL_THREADS;
+                    x[u] = e < nv ? ld_stream(vw + e) : PANEL_NONE;
+                    a[u] = e < nv ? ld_stream(va + e) : 0u;
                 }
             }
         }
