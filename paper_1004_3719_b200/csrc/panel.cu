@@ -156,7 +156,7 @@ __device__ __forceinline__ uint32_t addend(bool valued, uint32_t w, uint32_t a, 
 
 template <class IT, bool SPLIT, class VT>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
-k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ partial) {
+k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
     const PanelGeom g = op.g;
     IT *sx = reinterpret_cast<IT *>(smem);
@@ -167,38 +167,57 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
     const VT *vval = reinterpret_cast<const VT *>(op.vval);
     for (uint32_t i = threadIdx.x; i < ACC_STRIDE * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
     uint32_t cur_p = 0xFFFFFFFFu;
+    // Round 0 of both streams of the next tile is loaded before the current
+    // tile's write-out, so that write-out hides the next tile's first memory
+    // round trip.
+    uint32_t w[PBP], x[PBV], a[PBV];
+    uint32_t te0 = 0, tn = 0, tv0 = 0, tnv = 0;
+    auto prefetch = [&](uint32_t tt) {
+        te0 = op.tp[tt];
+        tn = op.tp[tt + 1] - te0;
+        tv0 = op.tv[tt];
+        tnv = op.tv[tt + 1] - tv0;
+        const uint32_t np = tn - tnv;
+        const uint32_t *pw = op.pent + te0, *vw = op.pent + te0 + np;
+        const VT *va = vval + tv0;
+#pragma unroll
+        for (int u = 0; u < PBP; ++u) {
+            const uint32_t e = u * PANEL_THREADS + threadIdx.x;
+            w[u] = e < np ? ld_stream(pw + e) : PANEL_NONE;
+        }
+#pragma unroll
+        for (int u = 0; u < PBV; ++u) {
+            const uint32_t e = u * PANEL_THREADS + threadIdx.x;
+            x[u] = e < tnv ? ld_stream(vw + e) : PANEL_NONE;
+            a[u] = e < tnv ? ld_stream(va + e) : 0u;
+        }
+    };
+    if (t0 < t1) prefetch(t0);
     for (uint32_t t = t0; t < t1; ++t) {
         const uint32_t p = t / g.B, b = t - p * g.B;
         if (p != cur_p) {
             const uint64_t c0 = (uint64_t)p * g.W;
             const uint32_t wn = (uint32_t)min((uint64_t)g.W, (uint64_t)op.cols - c0);
-            stage_x<IT>(sx, x, c0, wn);
+            stage_x<IT>(sx, xin, c0, wn);
             cur_p = p;
         }
         __syncthreads();
         // The +-1 part [0, np) and the valued part [np, n) of the tile run as
         // two specialised loops; every round issues all its loads before the
-        // first shared op, and the first valued round is loaded before the
-        // +-1 loop so the two streams share one memory round trip.
+        // first shared op.
         {
-            const uint32_t e0 = op.tp[t], n = op.tp[t + 1] - e0;
-            const uint32_t v0 = op.tv[t], nv = op.tv[t + 1] - v0, np = n - nv;
+            const uint32_t e0 = te0, n = tn;
+            const uint32_t v0 = tv0, nv = tnv, np = n - nv;
             const uint32_t *pw = op.pent + e0, *vw = op.pent + e0 + np;
             const VT *va = vval + v0;
             const uint32_t m = M.m;
-            uint32_t x[PBV], a[PBV];
-#pragma unroll
-            for (int u = 0; u < PBV; ++u) {
-                const uint32_t e = u * PANEL_THREADS + threadIdx.x;
-                x[u] = e < nv ? ld_stream(vw + e) : PANEL_NONE;
-                a[u] = e < nv ? ld_stream(va + e) : 0u;
-            }
             for (uint32_t base = threadIdx.x; base < np; base += PBP * PANEL_THREADS) {
-                uint32_t w[PBP];
+                if (base != threadIdx.x) {
 #pragma unroll
-                for (int u = 0; u < PBP; ++u) {
-                    const uint32_t e = base + u * PANEL_THREADS;
-                    w[u] = e < np ? ld_stream(pw + e) : PANEL_NONE;
+                    for (int u = 0; u < PBP; ++u) {
+                        const uint32_t e = base + u * PANEL_THREADS;
+                        w[u] = e < np ? ld_stream(pw + e) : PANEL_NONE;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < PBP; ++u) {
@@ -229,6 +248,7 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ x, IT *__restrict__ 
             }
         }
         __syncthreads();
+        if (t + 1 < t1) prefetch(t + 1);
         // one residue per band row -> partial[p][row]; re-zero the accumulators
         const uint64_t r0 = (uint64_t)b * g.R;
         const uint32_t rn = (uint32_t)min((uint64_t)g.R, (uint64_t)op.rows - r0);
