@@ -148,7 +148,7 @@ ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
         {h.pent.data(), h.pent.size() * 4, &p_pent},
         {h.vval.data(), h.vval.size(), &p_vval},
         {h.cta_t0.data(), h.cta_t0.size() * 4, &p_cta},
-        {nullptr, (size_t)h.g.P * h.rows * h.g.xbytes, &p_part},
+        {nullptr, (size_t)h.g.P * h.rows * 4, &p_part},
     };
     size_t total = 0;
     for (auto &pt : parts) total += a256(pt.bytes);
@@ -209,10 +209,10 @@ ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &devic
         if (o->strategy < 0 || o->strategy > 2)
             return fail(FFSPMV_ERR_INVALID_ARG, "strategy must be 0, 1 or 2");
         bo.strategy = o->strategy;
-        if (o->panel_rows && (o->panel_rows > PANEL_R_DEFAULT || o->panel_rows % 32))
-            return fail(FFSPMV_ERR_INVALID_ARG, "panel_rows must be a multiple of 32 <= 16320");
-        if (o->panel_cols && (o->panel_cols > 65536 || o->panel_cols % 32))
-            return fail(FFSPMV_ERR_INVALID_ARG, "panel_cols must be a multiple of 32 <= 65536");
+        if (o->panel_rows && (o->panel_rows > 32768 || o->panel_rows % 32))
+            return fail(FFSPMV_ERR_INVALID_ARG, "panel_rows must be a multiple of 32 <= 32768");
+        if (o->panel_cols && (o->panel_cols > 262144 || o->panel_cols % 32))
+            return fail(FFSPMV_ERR_INVALID_ARG, "panel_cols must be a multiple of 32 <= 262144");
         bo.panel_rows = o->panel_rows;
         bo.panel_cols = o->panel_cols;
     }

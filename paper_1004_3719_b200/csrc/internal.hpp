@@ -133,20 +133,18 @@ struct BuildOptions {
 // A tile writes one residue per band row into partial[p][row]; a reduction
 // pass sums the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
 // spmv(y, Ai, x); reduce(y, m)").
+// Packed entry word: col - p*W in bits [0, cb), sign in bit cb, row - b*R in
+// bits [cb+1, 32); cb = 18 / 16 / 16 for x staged as u8 / u16 / u32 (W =
+// 196608 / 65536 / 49152 columns, 192 / 128 / 192 KB), R = 8176 / 25312 / 4464
+// rows so that x panel + band accumulators fill the 227 KB of shared memory.
 struct Canon;
-constexpr uint32_t PANEL_COL_BITS = 16;
-constexpr uint32_t PANEL_SIGN = 1u << 16;
-constexpr uint32_t PANEL_ROW_SHIFT = 17;
-// Band rows: 14-bit row field, the top 64 slots are per-lane dummies that
-// absorb the masked-off lanes of a round without a branch.
-constexpr uint32_t PANEL_R_DEFAULT = 16384u - 64u;
-constexpr uint32_t PANEL_DUMMY_ROW = 16384u - 64u;
 
 struct PanelGeom {
     uint32_t W = 0, R = 0, P = 0, B = 0;
-    uint32_t xbytes = 4;       // bytes per staged x / partial element (1, 2, 4)
+    uint32_t xbytes = 4;       // bytes per staged x element (1, 2, 4)
     uint32_t split = 0;        // 1: accumulate residues as two u32 halves (m > 65536)
     uint32_t nctas = 0;        // persistent CTAs (one per SM)
+    uint32_t cb = 16;          // column bits of the packed word
 };
 
 struct HostPanel {
@@ -164,7 +162,7 @@ struct DevPanel {
     PanelGeom g;
     const uint32_t *tp, *tv, *pent, *vent, *cta_t0;
     const void *vval;
-    void *partial;                     // P * rows * xbytes scratch
+    void *partial;                     // P * rows u32 scratch
 };
 
 // Chooses W, R, element widths for modulus m.

@@ -10,12 +10,15 @@ namespace ffspmv {
 PanelGeom panel_geometry(uint64_t rows, uint64_t cols, uint32_t m, const BuildOptions &bo,
                          uint32_t nsm) {
     PanelGeom g;
-    // staged x element = partial element = narrowest type holding a residue
+    // staged x element = narrowest type holding a residue
     g.xbytes = m <= 256u ? 1 : m <= 65536u ? 2 : 4;
     g.split = m > 65536u ? 1 : 0;
-    // smem: W * xbytes (x panel) + R * 4 * (1 + split) (accumulators) <= 192 KB
-    g.W = g.xbytes == 4 ? 16384u : 65536u;
-    g.R = PANEL_R_DEFAULT;
+    // smem: W * xbytes (x panel) + R * 4 * (1 + split) (accumulators) <= 227 KB.
+    // Row sums must stay < 2^32 in a u32 accumulator: W * (m-1) < 2^32 for
+    // u8 (W = 196608) and u16 (W = 65536); SPLIT halves are < 2^16 each.
+    if (g.xbytes == 1) { g.W = 196608u; g.cb = 18; g.R = 8176u; }
+    else if (g.xbytes == 2) { g.W = 65536u; g.cb = 16; g.R = 25312u; }
+    else { g.W = 49152u; g.cb = 16; g.R = 4464u; }
     if (bo.panel_cols) g.W = std::min<uint32_t>(bo.panel_cols, g.W);
     if (bo.panel_rows) g.R = std::min<uint32_t>(bo.panel_rows, g.R);
     g.P = (uint32_t)((cols + g.W - 1) / g.W);
@@ -63,14 +66,14 @@ void pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &
     for (uint64_t t = 0; t < T; ++t) { pp[t] = hp.tp[t]; pv[t] = hp.tp[t] + npm[t]; pvv[t] = hp.tv[t]; }
     for (uint64_t r = 0; r < a.nrows; ++r) {
         uint64_t b = r / g.R;
-        uint32_t rl = (uint32_t)(r - b * g.R) << PANEL_ROW_SHIFT;
+        uint32_t rl = (uint32_t)(r - b * g.R) << (g.cb + 1);
         for (uint64_t t = a.ptr[r]; t < a.ptr[r + 1]; ++t) {
             uint32_t c = a.idx[t], v = a.val[t];
             uint64_t p = c / g.W;
             uint64_t tile = p * g.B + b;
             uint32_t word = rl | (uint32_t)(c - p * g.W);
             if (is_pm(v)) {
-                hp.pent[pp[tile]++] = word | (v == 1u ? 0u : PANEL_SIGN);
+                hp.pent[pp[tile]++] = word | (v == 1u ? 0u : (1u << g.cb));
             } else {
                 hp.pent[pv[tile]++] = word;
                 std::memcpy(&hp.vval[(uint64_t)(pvv[tile]++) * vb], &v, vb);
@@ -117,12 +120,12 @@ uint64_t reconstruct_panels(const HostPanel &hp, uint32_t m, uint32_t vb, uint32
             const uint32_t w = hp.pent[e], j = e - hp.tp[t];
             uint32_t v;
             if (j < np) {
-                v = (w & PANEL_SIGN) ? m - 1 : 1u;
+                v = (w & (1u << g.cb)) ? m - 1 : 1u;
             } else {
                 v = 0;
                 std::memcpy(&v, &hp.vval[(uint64_t)(hp.tv[t] + j - np) * vb], vb);
             }
-            emit((uint32_t)(b * g.R + (w >> PANEL_ROW_SHIFT)), (uint32_t)(p * g.W + (w & 0xFFFFu)), v);
+            emit((uint32_t)(b * g.R + (w >> (g.cb + 1))), (uint32_t)(p * g.W + (w & ((1u << g.cb) - 1))), v);
         }
     }
     return n;
