@@ -148,7 +148,7 @@ ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
         {h.pent.data(), h.pent.size() * 4, &p_pent},
         {h.vval.data(), h.vval.size(), &p_vval},
         {h.cta_t0.data(), h.cta_t0.size() * 4, &p_cta},
-        {nullptr, (size_t)h.g.P * h.rows * 4, &p_part},
+        {nullptr, (size_t)h.g.P * h.rows * h.g.xbytes, &p_part},
     };
     size_t total = 0;
     for (auto &pt : parts) total += a256(pt.bytes);

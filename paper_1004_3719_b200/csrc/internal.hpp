@@ -128,15 +128,14 @@ struct BuildOptions {
 // panels of W columns whose slice of x is staged in shared memory (the paper's
 // column-wise split of A, with x staged on chip); the rows into
 // bands of R rows whose accumulators live in shared memory.  Tile t = p*B + b
-// holds the entries of panel p x band b sorted by (row, col), each packed in
-// one u32:  col - p*W (bits 0..15) | sign (bit 16) | row - b*R (bits 17..30).
-// A tile writes one residue per band row into partial[p][row]; a reduction
-// pass sums the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
+// holds the entries of panel p x band b sorted by (row, col), its +-1 entries
+// first, each packed in one u32: col - p*W in bits [0, cb), sign in bit cb,
+// row - b*R in bits [cb+1, 32); cb = 18 / 16 / 16 for x staged as u8 / u16 /
+// u32 (W = 196608 / 65536 / 49152 columns = 192 / 128 / 192 KB of shared
+// memory, R = 8176 / 16320 / 4464 band rows of u32 accumulators).  A tile
+// writes one residue per band row into partial[p][row]; a reduction pass sums
+// the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
 // spmv(y, Ai, x); reduce(y, m)").
-// Packed entry word: col - p*W in bits [0, cb), sign in bit cb, row - b*R in
-// bits [cb+1, 32); cb = 18 / 16 / 16 for x staged as u8 / u16 / u32 (W =
-// 196608 / 65536 / 49152 columns, 192 / 128 / 192 KB), R = 8176 / 25312 / 4464
-// rows so that x panel + band accumulators fill the 227 KB of shared memory.
 struct Canon;
 
 struct PanelGeom {
@@ -162,7 +161,7 @@ struct DevPanel {
     PanelGeom g;
     const uint32_t *tp, *tv, *pent, *vent, *cta_t0;
     const void *vval;
-    void *partial;                     // P * rows u32 scratch
+    void *partial;                     // P * rows * xbytes scratch
 };
 
 // Chooses W, R, element widths for modulus m.

@@ -113,7 +113,7 @@ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t xv, const DevMod
 
 template <class IT, bool SPLIT, class VT>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
-k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, uint32_t *__restrict__ partial) {
+k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
     const PanelGeom g = op.g;
     IT *sx = reinterpret_cast<IT *>(smem);
@@ -206,19 +206,27 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, uint32_t *__res
         }
         __syncthreads();
         if (t + 1 < t1) prefetch(t + 1);
-        // one u32 per band row -> partial[p][row]; re-zero the accumulators.
-        // m <= 2^16: the raw sum (< W * m < 2^32), reduced mod m by the
-        // reduction pass; SPLIT: the residue of lo + hi * 2^16.
+        // one residue per band row -> partial[p][row] (same narrow type as the
+        // staged x); re-zero the accumulators.  m <= 2^16: the row sum is
+        // < W * m < 2^32 and reduces with the 32-bit Barrett; SPLIT: the
+        // residue of lo + hi * 2^16.
         const uint64_t r0 = (uint64_t)b * g.R;
         const uint32_t rn = (uint32_t)min((uint64_t)g.R, (uint64_t)op.rows - r0);
-        uint32_t *out = partial + (uint64_t)p * op.rows + r0;
+        IT *out = partial + (uint64_t)p * op.rows + r0;
         uint32_t r = 0;
-        if (!SPLIT && ((uintptr_t)out & 15) == 0) {
+        if (!SPLIT && ((uintptr_t)out % (4 * sizeof(IT))) == 0) {
             const uint32_t nq = rn / 4;
             for (uint32_t q = threadIdx.x; q < nq; q += PANEL_THREADS) {
                 const uint4 s4 = reinterpret_cast<const uint4 *>(acc)[q];
                 reinterpret_cast<uint4 *>(acc)[q] = make_uint4(0, 0, 0, 0);
-                st_keep4(out + 4 * q, s4);
+                const uint32_t v0 = mod32(s4.x, M), v1 = mod32(s4.y, M), v2 = mod32(s4.z, M),
+                               v3 = mod32(s4.w, M);
+                if constexpr (sizeof(IT) == 2) {
+                    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(out + 4 * q),
+                                 "r"(v0 | (v1 << 16)), "r"(v2 | (v3 << 16)), "l"(POLICY_EVICT_LAST));
+                } else {
+                    st_keep(reinterpret_cast<uint32_t *>(out + 4 * q), v0 | (v1 << 8) | (v2 << 16) | (v3 << 24));
+                }
             }
             r = nq * 4;
         }
@@ -228,32 +236,36 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, uint32_t *__res
                 res = mod64((uint64_t)acc[r] + ((uint64_t)acc[g.R + r] << 16), M);
                 acc[g.R + r] = 0;
             } else {
-                res = acc[r];
+                res = mod32(acc[r], M);
             }
             acc[r] = 0;
-            st_keep(out + r, res);
+            out[r] = (IT)res;
         }
         // the next tile's __syncthreads orders these writes before reuse
     }
 }
 
-// y[r] = alpha * sum_p partial[p][r] + beta * y[r]; four consecutive rows
-// per thread so each panel's partials load as one 16-byte vector.
-template <int VEC>
-__global__ void k_panel_reduce(const uint32_t *__restrict__ partial, uint32_t P, uint32_t rows,
+// y[r] = alpha * sum_p partial[p][r] + beta * y[r]; VEC = 16 / sizeof(IT)
+// consecutive rows per thread so each panel's partials load as one 16-byte
+// vector (VEC = 1 when rows is not a multiple of it).
+template <class IT, int VEC>
+__global__ void k_panel_reduce(const IT *__restrict__ partial, uint32_t P, uint32_t rows,
                                DevMod M, uint32_t alpha, uint32_t beta, uint32_t *__restrict__ y) {
     const uint32_t nvec = rows / VEC;
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
         uint64_t s[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) s[i] = 0;
-        for (uint32_t p = 0; p < P; ++p) {   // P u32 values < 2^32: exact in u64
-            const uint32_t *src = partial + (uint64_t)p * rows + (uint64_t)v * VEC;
-            if constexpr (VEC == 4) {
-                const uint4 e = *reinterpret_cast<const uint4 *>(src);
-                s[0] += e.x; s[1] += e.y; s[2] += e.z; s[3] += e.w;
+        for (uint32_t p = 0; p < P; ++p) {   // P residues < 2^32: exact in u64
+            const IT *src = partial + (uint64_t)p * rows + (uint64_t)v * VEC;
+            if constexpr (VEC * sizeof(IT) == 16) {
+                const uint4 e4 = *reinterpret_cast<const uint4 *>(src);
+                const IT *e = reinterpret_cast<const IT *>(&e4);
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) s[i] += e[i];
             } else {
-                s[0] += src[0];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) s[i] += src[i];
             }
         }
 #pragma unroll
@@ -269,7 +281,7 @@ template <class IT, bool SPLIT>
 int launch_t(const DevPanel &op, const DevMod &M, uint32_t alpha, const uint32_t *x, uint32_t beta,
              uint32_t *y, cudaStream_t st) {
     const PanelGeom &g = op.g;
-    uint32_t *partial = reinterpret_cast<uint32_t *>(op.partial);
+    IT *partial = reinterpret_cast<IT *>(op.partial);
     if (g.P > 0 && g.B > 0) {
         size_t smem = (size_t)g.W * sizeof(IT) + (size_t)g.R * 4 * (SPLIT ? 2 : 1);
         auto run = [&](auto kern) {
@@ -290,14 +302,15 @@ int launch_t(const DevPanel &op, const DevMod &M, uint32_t alpha, const uint32_t
         if (e) return e;
     }
     if (op.rows) {
-        // each panel's row block is 16-byte aligned only if rows % 4 == 0
-        const bool vec_ok = (op.rows % 4) == 0;
-        const uint32_t work = vec_ok ? op.rows / 4 : op.rows;
+        // each panel's row block is 16-byte aligned only if rows % VEC == 0
+        constexpr int VEC = 16 / sizeof(IT);
+        const bool vec_ok = (op.rows % VEC) == 0;
+        const uint32_t work = vec_ok ? op.rows / VEC : op.rows;
         const uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((work + 255) / 256, g.nctas * 8));
         if (vec_ok)
-            k_panel_reduce<4><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
+            k_panel_reduce<IT, VEC><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
         else
-            k_panel_reduce<1><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
+            k_panel_reduce<IT, 1><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
         count_launch();
     }
     return (int)cudaGetLastError();

@@ -17,7 +17,7 @@ PanelGeom panel_geometry(uint64_t rows, uint64_t cols, uint32_t m, const BuildOp
     // Row sums must stay < 2^32 in a u32 accumulator: W * (m-1) < 2^32 for
     // u8 (W = 196608) and u16 (W = 65536); SPLIT halves are < 2^16 each.
     if (g.xbytes == 1) { g.W = 196608u; g.cb = 18; g.R = 8176u; }
-    else if (g.xbytes == 2) { g.W = 65536u; g.cb = 16; g.R = 25312u; }
+    else if (g.xbytes == 2) { g.W = 65536u; g.cb = 16; g.R = 16320u; }
     else { g.W = 49152u; g.cb = 16; g.R = 4464u; }
     if (bo.panel_cols) g.W = std::min<uint32_t>(bo.panel_cols, g.W);
     if (bo.panel_rows) g.R = std::min<uint32_t>(bo.panel_rows, g.R);

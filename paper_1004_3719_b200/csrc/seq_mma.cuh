@@ -76,27 +76,11 @@ __global__ void k_seq_ufrag(const uint32_t *__restrict__ U, uint32_t ku, const u
     }
 }
 
-struct SmmaState {
-    int acc[4][SMMA_KMAX / 8][4];       // [limb combo][n-tile][frag]: hh, hl, lh, ll
-    unsigned long long p64[SMMA_KMAX / 8][4];
-    uint32_t since_fold;
-};
-
-__device__ __forceinline__ void smma_fold(SmmaState &st, int nt_count) {
-#pragma unroll
-    for (int nt = 0; nt < SMMA_KMAX / 8; ++nt) {
-        if (nt >= nt_count) break;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            st.p64[nt][e] += ((unsigned long long)(uint32_t)st.acc[0][nt][e] << 16) +
-                             (((unsigned long long)(uint32_t)st.acc[1][nt][e] +
-                               (uint32_t)st.acc[2][nt][e]) << 8) +
-                             (uint32_t)st.acc[3][nt][e];
-            st.acc[0][nt][e] = st.acc[1][nt][e] = st.acc[2][nt][e] = st.acc[3][nt][e] = 0;
-        }
-    }
-    st.since_fold = 0;
-}
+// Per-warp u64 projection accumulators live in shared memory,
+// p64[(nt*4 + e)*32 + lane] (lane-contiguous: conflict-free), so no
+// accumulator state stays in registers across slices: each slice's MMAs start
+// from zero and are folded into p64 right away.
+constexpr int SMMA_P64 = (SMMA_KMAX / 8) * 4 * 32;   // u64 per warp
 
 // SpMM of one SELL slice (u16 iterate, 4 columns per lane) + its projection.
 template <class Acc, class VT, int KPV>
@@ -105,7 +89,7 @@ __device__ __forceinline__ void seq_slice_mma(const DevOp &op, const DevMod &M, 
                                               const uint16_t *__restrict__ Vin,
                                               uint16_t *__restrict__ Vout,
                                               const uint32_t *__restrict__ ufrag,
-                                              uint8_t *vt, SmmaState &st) {
+                                              uint8_t *vt, unsigned long long *p64) {
     using S = SeqShape<KPV>;
     const uint32_t g = lane / KPV, cl = lane % KPV;
     const uint32_t col = cl * 4;
@@ -219,13 +203,20 @@ __device__ __forceinline__ void seq_slice_mma(const DevOp &op, const DevMod &M, 
             bh[jj] = *reinterpret_cast<const uint32_t *>(vt + off);
             bl[jj] = *reinterpret_cast<const uint32_t *>(vt + 32 * 32 + off);
         }
-        mma_u8(st.acc[0][nt], ah, bh);
-        mma_u8(st.acc[1][nt], ah, bl);
-        mma_u8(st.acc[2][nt], al, bh);
-        mma_u8(st.acc[3][nt], al, bl);
+        // U^T V = 2^16 Uh^T Vh + 2^8 (Uh^T Vl + Ul^T Vh) + Ul^T Vl; one slice
+        // adds at most 32 * 255^2 per element (x2 for the cross term): s32-exact
+        int hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
+        mma_u8(hh, ah, bh);
+        mma_u8(cr, ah, bl);
+        mma_u8(cr, al, bh);
+        mma_u8(ll, al, bl);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            p64[(nt * 4 + e) * 32 + lane] += ((unsigned long long)(uint32_t)hh[e] << 16) +
+                                             ((unsigned long long)(uint32_t)cr[e] << 8) +
+                                             (uint32_t)ll[e];
     }
     __syncwarp();
-    if (++st.since_fold == SMMA_FOLD) smma_fold(st, ntiles);
 }
 
 // Output policy of the scalar path inside the fused kernel: V_{t+1} and the
@@ -253,11 +244,13 @@ k_seq_step_mma(DevOp op, DevMod M, uint32_t k, uint32_t ku, const uint16_t *__re
                const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev) {
     __shared__ __align__(16) uint8_t vts[SMMA_WARPS][2 * 32 * 32];
     __shared__ unsigned long long pn[16 * SMMA_KMAX];
+    __shared__ unsigned long long p64s[SMMA_WARPS][SMMA_P64];
     __shared__ uint32_t red[SMMA_WARPS][16][SMMA_KMAX];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
     const uint32_t pairs = ku * k;
     for (uint32_t i = threadIdx.x; i < 16 * SMMA_KMAX; i += SMMA_WARPS * 32) pn[i] = 0;
+    for (uint32_t i = lane; i < SMMA_P64; i += 32) p64s[warp][i] = 0;
     __syncthreads();
     // finalise the previous step's S from its CTA partials
     for (uint32_t p = gw; part_prev && p < pairs; p += nw) {
@@ -266,18 +259,7 @@ k_seq_step_mma(DevOp op, DevMod M, uint32_t k, uint32_t ku, const uint16_t *__re
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
         if (lane == 0) S_prev[p] = mod64(s, M);
     }
-    SmmaState st;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int nt = 0; nt < SMMA_KMAX / 8; ++nt)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) st.acc[c][nt][e] = 0;
-#pragma unroll
-    for (int nt = 0; nt < SMMA_KMAX / 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) st.p64[nt][e] = 0;
-    st.since_fold = 0;
+    unsigned long long *p64 = p64s[warp];
     SeqScalarOut sout{Vout, U, k, ku, pn};
     const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
     for (uint32_t w = gw; w < items; w += nw) {
@@ -285,15 +267,14 @@ k_seq_step_mma(DevOp op, DevMod M, uint32_t k, uint32_t ku, const uint16_t *__re
             const uint32_t s = w - op.n_long;
             const SliceHdr h = load_hdr_b(op.slices + s);
             switch (h.regime) {
-                case ACC32: seq_slice_mma<Acc32, VT, KPV>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], st); break;
-                default: seq_slice_mma<Acc64, VT, KPV>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], st); break;
+                case ACC32: seq_slice_mma<Acc32, VT, KPV>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], p64); break;
+                default: seq_slice_mma<Acc64, VT, KPV>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], p64); break;
             }
         } else {
             block_item<VT, KP, 8>(op, M, w, lane, k, Vin, k, sout);
         }
     }
     const int ntiles = (int)((k + 7) / 8);
-    smma_fold(st, ntiles);
     // C fragment: element e of n-tile nt is (a = gid + 8*(e>>1), b = nt*8 + tig*2 + (e&1))
     const uint32_t gid = lane >> 2, tig = lane & 3;
 #pragma unroll
@@ -302,7 +283,7 @@ k_seq_step_mma(DevOp op, DevMod M, uint32_t k, uint32_t ku, const uint16_t *__re
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t a = gid + 8 * (e >> 1), b = nt * 8 + tig * 2 + (e & 1);
-            red[warp][a][b] = mod64(st.p64[nt][e], M);
+            red[warp][a][b] = mod64(p64[(nt * 4 + e) * 32 + lane], M);
         }
     }
     __syncthreads();
