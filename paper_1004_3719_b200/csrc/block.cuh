@@ -258,6 +258,34 @@ __device__ __forceinline__ void ld_vec(const TX *p, uint32_t (&v)[CPL]) {
     }
 }
 
+// Predicated vector gather (zeros when !pred) without a branch: the masked
+// lanes (slice padding, columns >= k) issue no memory request.
+template <class TX, int CPL>
+__device__ __forceinline__ void ld_vec_pred(const TX *p, bool pred, uint32_t (&v)[CPL]) {
+    uint32_t u[4] = {0, 0, 0, 0};
+    constexpr int BYTES = CPL * (int)sizeof(TX);
+    if constexpr (BYTES == 16) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+                     "@q ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+                     : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]) : "l"(p), "r"((uint32_t)pred));
+    } else if constexpr (BYTES == 8) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                     "@q ld.global.nc.v2.u32 {%0, %1}, [%2];\n\t}"
+                     : "+r"(u[0]), "+r"(u[1]) : "l"(p), "r"((uint32_t)pred));
+    } else {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                     "@q ld.global.nc.u32 %0, [%1];\n\t}"
+                     : "+r"(u[0]) : "l"(p), "r"((uint32_t)pred));
+    }
+    if constexpr (sizeof(TX) == 4) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) v[c] = u[c];
+    } else {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) v[c] = (u[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+    }
+}
+
 template <class Acc, class VT, int KPV, int NRMAX, int CPL, class TX, class Out>
 __device__ __forceinline__ void block_slice_vec(const DevOp &op, const DevMod &M, uint32_t s,
                                                 const SliceHdr &h, uint32_t lane, uint32_t k,
@@ -285,12 +313,8 @@ __device__ __forceinline__ void block_slice_vec(const DevOp &op, const DevMod &M
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i) {
                     cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
-                    if (cs[i] != PAD_COL && colok) {
-                        ld_vec<TX, CPL>(X + ((cs[i] & COL_MASK) * ldx + col), xv[i]);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) xv[i][c] = 0;
-                    }
+                    ld_vec_pred<TX, CPL>(X + ((cs[i] & COL_MASK) * ldx + col),
+                                         cs[i] != PAD_COL && colok, xv[i]);
                 }
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i)
@@ -308,12 +332,7 @@ __device__ __forceinline__ void block_slice_vec(const DevOp &op, const DevMod &M
                 for (int i = 0; i < S::NR; ++i) {
                     const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
                     as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i * S::G);
-                    if (c != PAD_COL && colok) {
-                        ld_vec<TX, CPL>(X + (c * ldx + col), xv[i]);
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < CPL; ++q) xv[i][q] = 0;
-                    }
+                    ld_vec_pred<TX, CPL>(X + (c * ldx + col), c != PAD_COL && colok, xv[i]);
                 }
 #pragma unroll
                 for (int i = 0; i < S::NR; ++i)

@@ -109,12 +109,8 @@ __device__ __forceinline__ void seq_slice_mma(const DevOp &op, const DevMod &M, 
 #pragma unroll
         for (int i = 0; i < S::NR; ++i) {
             cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i);
-            if (cs[i] != PAD_COL && colok) {
-                ld_vec<uint16_t, 4>(Vin + ((cs[i] & COL_MASK) * k + col), xv[i]);
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) xv[i][c] = 0;
-            }
+            ld_vec_pred<uint16_t, 4>(Vin + ((cs[i] & COL_MASK) * k + col), cs[i] != PAD_COL && colok,
+                                     xv[i]);
         }
 #pragma unroll
         for (int i = 0; i < S::NR; ++i)
@@ -131,12 +127,7 @@ __device__ __forceinline__ void seq_slice_mma(const DevOp &op, const DevMod &M, 
         for (int i = 0; i < S::NR; ++i) {
             const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i);
             as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i);
-            if (c != PAD_COL && colok) {
-                ld_vec<uint16_t, 4>(Vin + (c * k + col), xv[i]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) xv[i][q] = 0;
-            }
+            ld_vec_pred<uint16_t, 4>(Vin + (c * k + col), c != PAD_COL && colok, xv[i]);
         }
 #pragma unroll
         for (int i = 0; i < S::NR; ++i)
@@ -237,7 +228,7 @@ struct SeqScalarOut {
 };
 
 template <class VT, int KPV, int KP>
-__global__ void __launch_bounds__(SMMA_WARPS * 32)
+__global__ void __launch_bounds__(SMMA_WARPS * 32, 2)
 k_seq_step_mma(DevOp op, DevMod M, uint32_t k, uint32_t ku, const uint16_t *__restrict__ Vin,
                uint16_t *__restrict__ Vout, const uint32_t *__restrict__ U,
                const uint32_t *__restrict__ ufrag, uint32_t *__restrict__ part_out,
