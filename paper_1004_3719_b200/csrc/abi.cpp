@@ -141,14 +141,13 @@ ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
     d.rows = h.rows;
     d.cols = h.cols;
     d.g = h.g;
-    void *p_tp, *p_tv, *p_pent, *p_vval, *p_cta, *p_part;
+    void *p_tiles, *p_pent, *p_vval, *p_cta, *p_part;
     Part parts[] = {
-        {h.tp.data(), h.tp.size() * 4, &p_tp},
-        {h.tv.data(), h.tv.size() * 4, &p_tv},
+        {h.tiles.data(), h.tiles.size() * sizeof(PanelTile), &p_tiles},
         {h.pent.data(), h.pent.size() * 4, &p_pent},
         {h.vval.data(), h.vval.size(), &p_vval},
         {h.cta_t0.data(), h.cta_t0.size() * 4, &p_cta},
-        {nullptr, (size_t)h.g.P * h.rows * h.g.xbytes, &p_part},
+        {nullptr, (size_t)h.g.P * h.g.rows_pad * h.g.xbytes, &p_part},
     };
     size_t total = 0;
     for (auto &pt : parts) total += a256(pt.bytes);
@@ -166,10 +165,8 @@ ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
         }
         off += a256(pt.bytes);
     }
-    d.tp = (const uint32_t *)p_tp;
-    d.tv = (const uint32_t *)p_tv;
+    d.tiles = (const PanelTile *)p_tiles;
     d.pent = (const uint32_t *)p_pent;
-    d.vent = nullptr;
     d.vval = p_vval;
     d.cta_t0 = (const uint32_t *)p_cta;
     d.partial = p_part;
@@ -302,18 +299,17 @@ ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint3
         out.locality = gather_locality(ca);
         pack_operator(out.rows[0], ca, m, bo);   // block apply + sequence always use rows
         out.has_rows[0] = true;
-        if (choose_panels(ca, m, bo, nsm, out.locality)) {
-            pack_panels(out.pan[0], ca, m, bo, nsm);
-            out.has_pan[0] = true;
-        }
+        if (choose_panels(ca, m, bo, nsm, out.locality))
+            out.has_pan[0] = pack_panels(out.pan[0], ca, m, bo, nsm);
         if (want_t) {
             Canon ct;
             transpose_canon(ct, ca);
             ca = Canon();
-            if (choose_panels(ct, m, bo, nsm, gather_locality(ct))) {
-                pack_panels(out.pan[1], ct, m, bo, nsm);
+            if (choose_panels(ct, m, bo, nsm, gather_locality(ct)) &&
+                pack_panels(out.pan[1], ct, m, bo, nsm)) {
                 out.has_pan[1] = true;
             } else {
+                out.pan[1] = HostPanel();
                 pack_operator(out.rows[1], ct, m, bo);
                 out.has_rows[1] = true;
             }
@@ -323,7 +319,7 @@ ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint3
     }
     for (int k = 0; k < 2; ++k)
         if (out.rows[k].pcol.size() >= (1ull << 32) || out.rows[k].vcol.size() >= (1ull << 32) ||
-            out.pan[k].pent.size() >= (1ull << 32) || out.pan[k].vent.size() >= (1ull << 32))
+            out.pan[k].pent.size() >= (1ull << 32))
             return fail(FFSPMV_ERR_DIM, "packed streams exceed 2^32 slots");
     return FFSPMV_OK;
 }

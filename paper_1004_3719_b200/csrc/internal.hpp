@@ -128,13 +128,16 @@ struct BuildOptions {
 // panels of W columns whose slice of x is staged in shared memory (the paper's
 // column-wise split of A, with x staged on chip); the rows into
 // bands of R rows whose accumulators live in shared memory.  Tile t = p*B + b
-// holds the entries of panel p x band b sorted by (row, col), its +-1 entries
-// first, each packed in one u32: col - p*W in bits [0, cb), sign in bit cb,
-// row - b*R in bits [cb+1, 32); cb = 18 / 16 / 16 for x staged as u8 / u16 /
-// u32 (W = 196608 / 65536 / 49152 columns = 192 / 128 / 192 KB of shared
-// memory, R = 8176 / 16320 / 4464 band rows of u32 accumulators).  A tile
-// writes one residue per band row into partial[p][row]; a reduction pass sums
-// the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
+// holds the entries of panel p x band b in three sections -- +1 entries, -1
+// entries, valued entries -- each padded to a multiple of 4 ("quads") with a
+// dummy word that adds into the spare accumulator R.  An entry is one u32:
+// the byte offset of its column in the staged x panel, (col - p*W) * xbytes,
+// in bits [rs, 32), and its band row, row - b*R, in bits [0, rs); rs = 14 /
+// 15 / 14 for x staged as u8 / u16 / u32 (W = 196608 / 65536 / 49152 columns
+// = 192 / 128 / 192 KB of shared memory, R = 8176 / 16320 / 4464 band rows of
+// u32 accumulators).  A tile writes one residue per band row into
+// partial[p][row] (row stride rows_pad, a multiple of 16); a reduction pass
+// sums the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
 // spmv(y, Ai, x); reduce(y, m)").
 struct Canon;
 
@@ -143,15 +146,25 @@ struct PanelGeom {
     uint32_t xbytes = 4;       // bytes per staged x element (1, 2, 4)
     uint32_t split = 0;        // 1: accumulate residues as two u32 halves (m > 65536)
     uint32_t nctas = 0;        // persistent CTAs (one per SM)
-    uint32_t cb = 16;          // column bits of the packed word
+    uint32_t rs = 14;          // row bits of the packed word
+    uint32_t lazy = 0;         // 1: valued products enter the sum as Barrett remainders < 2m
+    uint32_t rows_pad = 0;     // partial row stride (rows rounded up to 16)
 };
+
+// One tile: quads [q0, q0 + nqp) are +1 entries, the next nqm quads -1
+// entries, the next nqv quads valued entries whose values are value quads
+// [vq0, vq0 + nqv).  p, b: panel and band; rn: live band rows.
+struct PanelTile {
+    uint32_t q0, nqp, nqm, nqv, vq0, p, b, rn;
+};
+static_assert(sizeof(PanelTile) == 32, "PanelTile is 32 bytes");
 
 struct HostPanel {
     uint32_t rows = 0, cols = 0;
     PanelGeom g;
-    std::vector<uint32_t> tp, tv;      // tile entry / value offsets, P*B + 1 each
-    std::vector<uint32_t> pent, vent;  // pent: packed entries (per tile: +-1 then valued); vent unused
-    std::vector<uint8_t> vval;         // values of the valued entries (vbytes each)
+    std::vector<PanelTile> tiles;      // P*B tiles, panel-major
+    std::vector<uint32_t> pent;        // packed entries, 4 per quad
+    std::vector<uint8_t> vval;         // values of the valued quads (4 * vbytes per quad)
     std::vector<uint32_t> cta_t0;      // nctas + 1 tile boundaries
     uint64_t nnz_pm = 0, nnz_val = 0, stream_bytes = 0;
 };
@@ -159,15 +172,18 @@ struct HostPanel {
 struct DevPanel {
     uint32_t rows, cols;
     PanelGeom g;
-    const uint32_t *tp, *tv, *pent, *vent, *cta_t0;
+    const PanelTile *tiles;
+    const uint32_t *pent, *cta_t0;
     const void *vval;
-    void *partial;                     // P * rows * xbytes scratch
+    void *partial;                     // P * rows_pad * xbytes scratch
 };
 
 // Chooses W, R, element widths for modulus m.
 PanelGeom panel_geometry(uint64_t rows, uint64_t cols, uint32_t m, const BuildOptions &bo,
                          uint32_t nsm);
-void pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &bo, uint32_t nsm);
+// false when a tile row's sum could overflow its u32 accumulator (the caller
+// then keeps the rows layout).
+bool pack_panels(HostPanel &hp, const Canon &a, uint32_t m, const BuildOptions &bo, uint32_t nsm);
 uint64_t reconstruct_panels(const HostPanel &hp, uint32_t m, uint32_t vbytes, uint32_t *rr,
                             uint32_t *rc, uint32_t *rv, uint64_t cap);
 // Column-locality of the rows layout: distinct 128 B x lines touched per

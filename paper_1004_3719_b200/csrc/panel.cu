@@ -25,31 +25,38 @@ void count_launch();
 namespace {
 
 constexpr int PANEL_THREADS = 1024;
-constexpr int PBP = 4;  // +-1 entries per thread per round (all loads issued first)
-constexpr int PBV = 8;  // valued entries per thread per round
-constexpr uint32_t PANEL_NONE = 0xFFFFFFFFu;  // no entry (a packed word never has row >= R)
+
+// Shared memory: x panel (W * sizeof(IT)) | accumulators ((R + 1) u32, twice
+// when SPLIT) | tile-header cache (HC headers, 16-byte aligned).
+template <bool SPLIT>
+__host__ __device__ constexpr uint32_t panel_hc() { return SPLIT ? 16u : 64u; }
+template <class IT, bool SPLIT>
+__host__ __device__ __forceinline__ size_t hc_offset(const PanelGeom &g) {
+    return ((size_t)g.W * sizeof(IT) + (size_t)(g.R + 1) * 4 * (SPLIT ? 2 : 1) + 15) / 16 * 16;
+}
 
 // Shared-memory accesses through 32-bit shared addresses (no generic-address
-// conversion in the hot loop).
+// conversion in the hot loop).  `off` is a byte offset.
 template <class IT>
-__device__ __forceinline__ uint32_t lds_x(uint32_t base, uint32_t i) {
+__device__ __forceinline__ uint32_t lds_x(uint32_t base, uint32_t off) {
     uint32_t v;
     if constexpr (sizeof(IT) == 1) {
         unsigned short h;
-        asm volatile("ld.shared.u8 %0, [%1];" : "=h"(h) : "r"(base + i));
+        asm volatile("ld.shared.u8 %0, [%1];" : "=h"(h) : "r"(base + off));
         v = h;
     } else if constexpr (sizeof(IT) == 2) {
         unsigned short h;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + 2 * i));
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(base + off));
         v = h;
     } else {
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + 4 * i));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + off));
     }
     return v;
 }
 
-// acc[row] += v (two u32 halves at acc and acc + R when SPLIT: each half of
-// a residue < 2^32 is < 2^16, and a tile row has at most W < 2^16 addends)
+// acc[row] += v (two u32 halves at acc and acc + hi_off when SPLIT: each half
+// of a residue <= m < 2^32 is < 2^16, and a tile row has at most W < 2^16
+// addends)
 template <bool SPLIT>
 __device__ __forceinline__ void acc_add_s(uint32_t acc_s, uint32_t hi_off, uint32_t row, uint32_t v) {
     if constexpr (SPLIT) {
@@ -60,18 +67,52 @@ __device__ __forceinline__ void acc_add_s(uint32_t acc_s, uint32_t hi_off, uint3
     }
 }
 
-// partial stores stay in L2 for the reduction pass
-__device__ __forceinline__ void st_keep4(uint32_t *p, uint4 v) {
-    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
-                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(POLICY_EVICT_LAST));
+// Stream quads: read once -> no L1 allocation, evict-first in L2.  Out of
+// range (pred false) -> `dflt` in every lane, which the kernel treats as a
+// padding word.
+__device__ __forceinline__ uint4 ld_quad(const uint4 *p, bool pred, uint32_t dflt) {
+    uint4 v = make_uint4(dflt, dflt, dflt, dflt);
+    asm volatile(
+        "{.reg .pred q; setp.ne.u32 q, %5, 0;\n"
+        "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %6;}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "l"(p), "r"((uint32_t)pred), "l"(POLICY_EVICT_FIRST));
+    return v;
 }
-__device__ __forceinline__ void st_keep(uint32_t *p, uint32_t v) {
-    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v),
-                 "l"(POLICY_EVICT_LAST));
+// Raw values of one valued quad (4 x IT packed into .x / .x,.y / .x..w),
+// 0 when pred is false; unpacked with vals().
+template <class IT>
+__device__ __forceinline__ uint4 ld_vraw(const void *base, uint64_t vq, bool pred) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if constexpr (sizeof(IT) == 1) {
+        asm volatile("{.reg .pred q; setp.ne.u32 q, %2, 0;\n"
+                     "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %3;}"
+                     : "+r"(v.x) : "l"(reinterpret_cast<const uint32_t *>(base) + vq), "r"((uint32_t)pred),
+                       "l"(POLICY_EVICT_FIRST));
+    } else if constexpr (sizeof(IT) == 2) {
+        asm volatile("{.reg .pred q; setp.ne.u32 q, %3, 0;\n"
+                     "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %4;}"
+                     : "+r"(v.x), "+r"(v.y) : "l"(reinterpret_cast<const uint2 *>(base) + vq), "r"((uint32_t)pred),
+                       "l"(POLICY_EVICT_FIRST));
+    } else {
+        v = ld_quad(reinterpret_cast<const uint4 *>(base) + vq, pred, 0u);
+    }
+    return v;
+}
+template <class IT>
+__device__ __forceinline__ void vals(const uint4 &v, uint32_t (&a)[4]) {
+    if constexpr (sizeof(IT) == 1) {
+        a[0] = v.x & 0xFFu; a[1] = (v.x >> 8) & 0xFFu; a[2] = (v.x >> 16) & 0xFFu; a[3] = v.x >> 24;
+    } else if constexpr (sizeof(IT) == 2) {
+        a[0] = v.x & 0xFFFFu; a[1] = v.x >> 16; a[2] = v.y & 0xFFFFu; a[3] = v.y >> 16;
+    } else {
+        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+    }
 }
 
 // x panel -> shared memory, converted to the narrow staged type.  Eight
-// 16-byte loads per thread are issued before any store.
+// 16-byte loads per thread are issued before any store; four residues pack
+// into one 4-byte (u8) or 8-byte (u16) shared store.
 template <class IT>
 __device__ __forceinline__ void stage_x(IT *sx, const uint32_t *__restrict__ x, uint64_t c0,
                                         uint32_t wn) {
@@ -92,10 +133,15 @@ __device__ __forceinline__ void stage_x(IT *sx, const uint32_t *__restrict__ x, 
             for (int u = 0; u < U; ++u) {
                 const uint32_t i = base + u * PANEL_THREADS;
                 if (i < nvec) {
-                    sx[4 * i] = (IT)v[u].x;
-                    sx[4 * i + 1] = (IT)v[u].y;
-                    sx[4 * i + 2] = (IT)v[u].z;
-                    sx[4 * i + 3] = (IT)v[u].w;
+                    if constexpr (sizeof(IT) == 1) {
+                        reinterpret_cast<uint32_t *>(sx)[i] =
+                            __byte_perm(__byte_perm(v[u].x, v[u].y, 0x0040), __byte_perm(v[u].z, v[u].w, 0x0040), 0x5410);
+                    } else if constexpr (sizeof(IT) == 2) {
+                        reinterpret_cast<uint2 *>(sx)[i] =
+                            make_uint2(__byte_perm(v[u].x, v[u].y, 0x5410), __byte_perm(v[u].z, v[u].w, 0x5410));
+                    } else {
+                        reinterpret_cast<uint4 *>(sx)[i] = v[u];
+                    }
                 }
             }
         }
@@ -104,14 +150,51 @@ __device__ __forceinline__ void stage_x(IT *sx, const uint32_t *__restrict__ x, 
     for (uint32_t i = done + threadIdx.x; i < wn; i += PANEL_THREADS) sx[i] = (IT)__ldg(src + i);
 }
 
-// (a * x) mod m of a valued entry, in 32-bit arithmetic when m <= 2^16
-template <bool SPLIT>
-__device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t xv, const DevMod &M) {
-    if constexpr (SPLIT) return mod64((uint64_t)a * xv, M);
-    else return mod32(a * xv, M);
+// x mod m for x < 2^32, m <= 2^16: Barrett remainder r in [0, 2m), then
+// min(r, r - m) as unsigned (r - m wraps to a huge value when r < m).
+__device__ __forceinline__ uint32_t mod32_min(uint32_t x, const DevMod &M) {
+    const uint32_t r = __umulhi(x, M.mu32) * (0u - M.m) + x;
+    return min(r, r - M.m);
 }
 
-template <class IT, bool SPLIT, class VT>
+// (a * x) mod m of a valued entry.  LAZY: the Barrett remainder before its
+// correction, in [0, 2m) (mod32's argument; the builder checked that a tile
+// row's sum of such terms stays < 2^32).
+template <bool SPLIT, bool LAZY>
+__device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t xv, const DevMod &M) {
+    if constexpr (SPLIT) return mod64((uint64_t)a * xv, M);
+    else if constexpr (LAZY) {
+        const uint32_t p = a * xv;
+        return __umulhi(p, M.mu32) * (0u - M.m) + p;
+    } else return mod32(a * xv, M);
+}
+
+// Processing of one quad of the tile; kind 0 / 1 / 2 = +1 / -1 / valued.
+template <class IT, bool SPLIT, bool LAZY>
+__device__ __forceinline__ void do_quad(uint32_t kind, const uint4 &w, const uint4 &raw,
+                                        uint32_t sx_s, uint32_t acc_s, uint32_t hi_off, uint32_t rs,
+                                        uint32_t rmask, const DevMod &M) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    if (kind == 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            acc_add_s<SPLIT>(acc_s, hi_off, ws[u] & rmask, lds_x<IT>(sx_s, ws[u] >> rs));
+    } else if (kind == 1) {
+        // m - x <= m (x = 0 adds m: a multiple of m, harmless)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            acc_add_s<SPLIT>(acc_s, hi_off, ws[u] & rmask, M.m - lds_x<IT>(sx_s, ws[u] >> rs));
+    } else {
+        uint32_t a[4];
+        vals<IT>(raw, a);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            acc_add_s<SPLIT>(acc_s, hi_off, ws[u] & rmask,
+                             mulmod<SPLIT, LAZY>(a[u], lds_x<IT>(sx_s, ws[u] >> rs), M));
+    }
+}
+
+template <class IT, bool SPLIT, bool LAZY>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
 k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -120,126 +203,130 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict_
     uint32_t *acc = reinterpret_cast<uint32_t *>(smem + (size_t)g.W * sizeof(IT));
     const uint32_t sx_s = (uint32_t)__cvta_generic_to_shared(sx);
     const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);
-    const uint32_t hi_off = 4 * g.R;                 // SPLIT: high halves at acc + R
-    const uint32_t colmask = (1u << g.cb) - 1, signbit = 1u << g.cb, rshift = g.cb + 1;
+    const uint32_t hi_off = 4 * (g.R + 1);           // SPLIT: high halves after the low ones
+    const uint32_t rs = g.rs, rmask = (1u << g.rs) - 1, dummy = g.R;
     const uint32_t t0 = op.cta_t0[blockIdx.x], t1 = op.cta_t0[blockIdx.x + 1];
-    const VT *vval = reinterpret_cast<const VT *>(op.vval);
-    for (uint32_t i = threadIdx.x; i < g.R * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
+    const uint4 *pq = reinterpret_cast<const uint4 *>(op.pent);
+    const uint32_t tid = threadIdx.x;
+    constexpr uint32_t HC = panel_hc<SPLIT>();
+    for (uint32_t i = tid; i < (g.R + 1) * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
     uint32_t cur_p = 0xFFFFFFFFu;
-    // Round 0 of both streams of the next tile is loaded before the current
-    // tile's write-out, so that write-out hides the next tile's first memory
-    // round trip.
-    uint32_t w[PBP], x[PBV], a[PBV];
-    uint32_t te0 = 0, tn = 0, tv0 = 0, tnv = 0;
-    auto prefetch = [&](uint32_t tt) {
-        te0 = op.tp[tt];
-        tn = op.tp[tt + 1] - te0;
-        tv0 = op.tv[tt];
-        tnv = op.tv[tt + 1] - tv0;
-        const uint32_t np = tn - tnv;
-        const uint32_t *pw = op.pent + te0, *vw = op.pent + te0 + np;
-        const VT *va = vval + tv0;
+    // Software pipeline over the CTA's tiles: the headers sit in shared
+    // memory, and the first QR quads per thread of tile t+1 (the
+    // whole tile when it has <= QR * 1024 quads) are loaded into registers
+    // before tile t's write-out, so the stream latency hides behind it.
+    constexpr int QR = SPLIT ? 2 : 4;
+    uint4 rw[QR], ra[QR];
+    auto load_regs = [&](const PanelTile &T) {
+        const uint32_t nq = T.nqp + T.nqm + T.nqv, ev = T.nqp + T.nqm;
 #pragma unroll
-        for (int u = 0; u < PBP; ++u) {
-            const uint32_t e = u * PANEL_THREADS + threadIdx.x;
-            w[u] = e < np ? ld_stream(pw + e) : PANEL_NONE;
-        }
-#pragma unroll
-        for (int u = 0; u < PBV; ++u) {
-            const uint32_t e = u * PANEL_THREADS + threadIdx.x;
-            x[u] = e < tnv ? ld_stream(vw + e) : PANEL_NONE;
-            a[u] = e < tnv ? ld_stream(va + e) : 0u;
+        for (int i = 0; i < QR; ++i) {
+            const uint32_t q = tid + i * PANEL_THREADS;
+            if (q < nq) {
+                rw[i] = ld_quad(pq + T.q0 + q, true, dummy);
+                ra[i] = ld_vraw<IT>(op.vval, (uint64_t)T.vq0 + (q - ev), q >= ev);
+            }
         }
     };
-    if (t0 < t1) prefetch(t0);
+    // tile headers of the CTA's range, HC at a time, in shared memory
+    PanelTile *hc = reinterpret_cast<PanelTile *>(smem + hc_offset<IT, SPLIT>(g));
+    auto fill_hc = [&](uint32_t tb) {
+        for (uint32_t i = tid; i < 2 * HC; i += PANEL_THREADS)
+            if (tb + i / 2 < t1)
+                reinterpret_cast<uint4 *>(hc)[i] = __ldg(reinterpret_cast<const uint4 *>(op.tiles + tb) + i);
+    };
+    // the current header is read from shared memory where it is used (no
+    // registers held across the tile)
+    uint32_t jc = 0;
+    if (t0 < t1) {
+        fill_hc(t0);
+        __syncthreads();
+        load_regs(hc[0]);
+    }
     for (uint32_t t = t0; t < t1; ++t) {
-        const uint32_t p = t / g.B, b = t - p * g.B;
-        if (p != cur_p) {
-            const uint64_t c0 = (uint64_t)p * g.W;
+        const PanelTile &T = hc[jc];
+        if (T.p != cur_p) {
+            const uint64_t c0 = (uint64_t)T.p * g.W;
             const uint32_t wn = (uint32_t)min((uint64_t)g.W, (uint64_t)op.cols - c0);
             stage_x<IT>(sx, xin, c0, wn);
-            cur_p = p;
+            cur_p = T.p;
         }
         __syncthreads();
-        // The +-1 part [0, np) and the valued part [np, n) of the tile run as
-        // two specialised loops; every round issues all its loads before the
-        // first shared op.
         {
-            const uint32_t np = tn - tnv, nv = tnv;
-            const uint32_t *pw = op.pent + te0, *vw = op.pent + te0 + np;
-            const VT *va = vval + tv0;
-            const uint32_t m = M.m;
-            for (uint32_t base = threadIdx.x; base < np; base += PBP * PANEL_THREADS) {
-                if (base != threadIdx.x) {
+            const uint32_t e1 = T.nqp, e2 = T.nqp + T.nqm, nq = e2 + T.nqv;
 #pragma unroll
-                    for (int u = 0; u < PBP; ++u) {
-                        const uint32_t e = base + u * PANEL_THREADS;
-                        w[u] = e < np ? ld_stream(pw + e) : PANEL_NONE;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < PBP; ++u) {
-                    if (w[u] != PANEL_NONE) {
-                        const uint32_t xv = lds_x<IT>(sx_s, w[u] & colmask);
-                        const uint32_t ad = (w[u] & signbit) ? (xv ? m - xv : 0u) : xv;
-                        acc_add_s<SPLIT>(acc_s, hi_off, w[u] >> rshift, ad);
-                    }
-                }
+            for (int i = 0; i < QR; ++i) {
+                const uint32_t q = tid + i * PANEL_THREADS;
+                if (q < nq)
+                    do_quad<IT, SPLIT, LAZY>(q < e1 ? 0u : q < e2 ? 1u : 2u, rw[i], ra[i], sx_s, acc_s,
+                                             hi_off, rs, rmask, M);
             }
-            for (uint32_t base = threadIdx.x; base < nv;) {
-#pragma unroll
-                for (int u = 0; u < PBV; ++u) {
-                    if (x[u] != PANEL_NONE) {
-                        const uint32_t xv = lds_x<IT>(sx_s, x[u] & colmask);
-                        acc_add_s<SPLIT>(acc_s, hi_off, x[u] >> rshift, mulmod<SPLIT>(a[u], xv, M));
-                    }
-                }
-                base += PBV * PANEL_THREADS;
-                if (base >= nv) break;
-#pragma unroll
-                for (int u = 0; u < PBV; ++u) {
-                    const uint32_t e = base + u * PANEL_THREADS;
-                    x[u] = e < nv ? ld_stream(vw + e) : PANEL_NONE;
-                    a[u] = e < nv ? ld_stream(va + e) : 0u;
-                }
+            // quads beyond the register ring: two per thread per round
+            for (uint32_t q = tid + QR * PANEL_THREADS; q < nq; q += 2 * PANEL_THREADS) {
+                const uint32_t qb = q + PANEL_THREADS;
+                const uint4 w0 = ld_quad(pq + T.q0 + q, true, dummy);
+                const uint4 w1 = ld_quad(pq + T.q0 + qb, qb < nq, dummy);
+                const uint4 a0 = ld_vraw<IT>(op.vval, (uint64_t)T.vq0 + (q - e2), q >= e2);
+                const uint4 a1 = ld_vraw<IT>(op.vval, (uint64_t)T.vq0 + (qb - e2), qb >= e2 && qb < nq);
+                do_quad<IT, SPLIT, LAZY>(q < e1 ? 0u : q < e2 ? 1u : 2u, w0, a0, sx_s, acc_s, hi_off, rs, rmask, M);
+                if (qb < nq)
+                    do_quad<IT, SPLIT, LAZY>(qb < e1 ? 0u : qb < e2 ? 1u : 2u, w1, a1, sx_s, acc_s, hi_off, rs,
+                                             rmask, M);
             }
         }
+        // read before the barrier: after it, fill_hc may overwrite the cache
+        const uint32_t p = T.p, b = T.b, rn = T.rn;
         __syncthreads();
-        if (t + 1 < t1) prefetch(t + 1);
+        if (t + 1 < t1) {
+            const uint32_t j = (t + 1 - t0) % HC;
+            if (j == 0) {            // next chunk of headers (uniform branch)
+                fill_hc(t + 1);
+                __syncthreads();
+            }
+            jc = j;
+            load_regs(hc[j]);
+        }
         // one residue per band row -> partial[p][row] (same narrow type as the
-        // staged x); re-zero the accumulators.  m <= 2^16: the row sum is
-        // < W * m < 2^32 and reduces with the 32-bit Barrett; SPLIT: the
-        // residue of lo + hi * 2^16.
-        const uint64_t r0 = (uint64_t)b * g.R;
-        const uint32_t rn = (uint32_t)min((uint64_t)g.R, (uint64_t)op.rows - r0);
-        IT *out = partial + (uint64_t)p * op.rows + r0;
-        uint32_t r = 0;
-        if (!SPLIT && ((uintptr_t)out % (4 * sizeof(IT))) == 0) {
-            const uint32_t nq = rn / 4;
-            for (uint32_t q = threadIdx.x; q < nq; q += PANEL_THREADS) {
-                const uint4 s4 = reinterpret_cast<const uint4 *>(acc)[q];
-                reinterpret_cast<uint4 *>(acc)[q] = make_uint4(0, 0, 0, 0);
-                const uint32_t v0 = mod32(s4.x, M), v1 = mod32(s4.y, M), v2 = mod32(s4.z, M),
-                               v3 = mod32(s4.w, M);
-                if constexpr (sizeof(IT) == 2) {
-                    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(out + 4 * q),
-                                 "r"(v0 | (v1 << 16)), "r"(v2 | (v3 << 16)), "l"(POLICY_EVICT_LAST));
+        // staged x); re-zero the accumulators.  Four rows per thread per step:
+        // one conflict-free 16-byte shared load (lanes read consecutive
+        // vectors) and one 4 * sizeof(IT)-byte store.  Without SPLIT the row
+        // sum is < 2^32 (checked by the builder) and reduces with the 32-bit
+        // Barrett; SPLIT: the residue of lo + hi * 2^16.  Rows rn ..
+        // round16(rn) hold zeros (no entries) and land in the padding.
+        IT *out = partial + (uint64_t)p * g.rows_pad + (uint64_t)b * g.R;
+        const uint32_t nv = (rn + 3) / 4;
+        for (uint32_t v = tid; v < nv; v += PANEL_THREADS) {
+            const uint4 s4 = reinterpret_cast<const uint4 *>(acc)[v];
+            reinterpret_cast<uint4 *>(acc)[v] = make_uint4(0, 0, 0, 0);
+            uint32_t res[4];
+            if constexpr (SPLIT) {
+                const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t r = 4 * v + i;
+                    res[i] = mod64((uint64_t)sv[i] + ((uint64_t)acc[g.R + 1 + r] << 16), M);
+                    acc[g.R + 1 + r] = 0;
+                }
+                asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(
+                                 reinterpret_cast<uint4 *>(out) + v),
+                             "r"(res[0]), "r"(res[1]), "r"(res[2]), "r"(res[3]), "l"(POLICY_EVICT_LAST));
+            } else {
+                res[0] = mod32_min(s4.x, M);
+                res[1] = mod32_min(s4.y, M);
+                res[2] = mod32_min(s4.z, M);
+                res[3] = mod32_min(s4.w, M);
+                if constexpr (sizeof(IT) == 1) {
+                    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(
+                                     reinterpret_cast<uint32_t *>(out) + v),
+                                 "r"(__byte_perm(__byte_perm(res[0], res[1], 0x0040), __byte_perm(res[2], res[3], 0x0040), 0x5410)),
+                                 "l"(POLICY_EVICT_LAST));
                 } else {
-                    st_keep(reinterpret_cast<uint32_t *>(out + 4 * q), v0 | (v1 << 8) | (v2 << 16) | (v3 << 24));
+                    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(
+                                     reinterpret_cast<uint2 *>(out) + v),
+                                 "r"(__byte_perm(res[0], res[1], 0x5410)), "r"(__byte_perm(res[2], res[3], 0x5410)),
+                                 "l"(POLICY_EVICT_LAST));
                 }
             }
-            r = nq * 4;
-        }
-        for (r += threadIdx.x; r < rn; r += PANEL_THREADS) {
-            uint32_t res;
-            if constexpr (SPLIT) {
-                res = mod64((uint64_t)acc[r] + ((uint64_t)acc[g.R + r] << 16), M);
-                acc[g.R + r] = 0;
-            } else {
-                res = mod32(acc[r], M);
-            }
-            acc[r] = 0;
-            out[r] = (IT)res;
         }
         // the next tile's __syncthreads orders these writes before reuse
     }
@@ -247,34 +334,60 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict_
 
 // y[r] = alpha * sum_p partial[p][r] + beta * y[r]; VEC = 16 / sizeof(IT)
 // consecutive rows per thread so each panel's partials load as one 16-byte
-// vector (VEC = 1 when rows is not a multiple of it).
-template <class IT, int VEC>
+// vector (the partial row stride is a multiple of 16).
+template <class IT>
 __global__ void k_panel_reduce(const IT *__restrict__ partial, uint32_t P, uint32_t rows,
-                               DevMod M, uint32_t alpha, uint32_t beta, uint32_t *__restrict__ y) {
-    const uint32_t nvec = rows / VEC;
+                               uint32_t rows_pad, DevMod M, uint32_t alpha, uint32_t beta,
+                               uint32_t *__restrict__ y, bool y_aligned) {
+    constexpr int VEC = 16 / sizeof(IT);
+    const uint32_t nvec = (rows + VEC - 1) / VEC;
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
         uint64_t s[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) s[i] = 0;
         for (uint32_t p = 0; p < P; ++p) {   // P residues < 2^32: exact in u64
-            const IT *src = partial + (uint64_t)p * rows + (uint64_t)v * VEC;
-            if constexpr (VEC * sizeof(IT) == 16) {
-                const uint4 e4 = *reinterpret_cast<const uint4 *>(src);
-                const IT *e = reinterpret_cast<const IT *>(&e4);
+            const uint4 e4 = __ldcs(reinterpret_cast<const uint4 *>(partial + (uint64_t)p * rows_pad) + v);
+            const IT *e = reinterpret_cast<const IT *>(&e4);
 #pragma unroll
-                for (int i = 0; i < VEC; ++i) s[i] += e[i];
-            } else {
+            for (int i = 0; i < VEC; ++i) s[i] += e[i];
+        }
+        const uint32_t r0 = v * VEC;
+        if (y_aligned && r0 + VEC <= rows) {
 #pragma unroll
-                for (int i = 0; i < VEC; ++i) s[i] += src[i];
+            for (int i = 0; i < VEC; i += 4) {
+                uint4 yo = beta ? *reinterpret_cast<const uint4 *>(y + r0 + i) : make_uint4(0, 0, 0, 0);
+                yo.x = epilogue(mod64(s[i], M), alpha, beta, yo.x, M);
+                yo.y = epilogue(mod64(s[i + 1], M), alpha, beta, yo.y, M);
+                yo.z = epilogue(mod64(s[i + 2], M), alpha, beta, yo.z, M);
+                yo.w = epilogue(mod64(s[i + 3], M), alpha, beta, yo.w, M);
+                *reinterpret_cast<uint4 *>(y + r0 + i) = yo;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) {
+                const uint32_t r = r0 + i;
+                if (r < rows) {
+                    const uint32_t yold = beta ? y[r] : 0u;
+                    y[r] = epilogue(mod64(s[i], M), alpha, beta, yold, M);
+                }
             }
         }
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) {
-            const uint32_t r = v * VEC + i;
-            const uint32_t yold = beta ? y[r] : 0u;
-            y[r] = epilogue(mod64(s[i], M), alpha, beta, yold, M);
-        }
     }
+}
+
+// one static per kernel instantiation: the dynamic-smem opt-in is per function
+template <class IT, bool SPLIT, bool LAZY>
+void run_panel(const DevPanel &op, const DevMod &M, const uint32_t *x, IT *partial, size_t smem,
+               cudaStream_t st) {
+    static size_t configured[64] = {};     // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    size_t &c = configured[dev & 63];
+    if (c < smem) {
+        cudaFuncSetAttribute(k_panel<IT, SPLIT, LAZY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        c = smem;
+    }
+    k_panel<IT, SPLIT, LAZY><<<op.g.nctas, PANEL_THREADS, smem, st>>>(op, M, x, partial);
 }
 
 template <class IT, bool SPLIT>
@@ -283,34 +396,20 @@ int launch_t(const DevPanel &op, const DevMod &M, uint32_t alpha, const uint32_t
     const PanelGeom &g = op.g;
     IT *partial = reinterpret_cast<IT *>(op.partial);
     if (g.P > 0 && g.B > 0) {
-        size_t smem = (size_t)g.W * sizeof(IT) + (size_t)g.R * 4 * (SPLIT ? 2 : 1);
-        auto run = [&](auto kern) {
-            static size_t configured = 0;   // per instantiation
-            if (configured < smem) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                configured = smem;
-            }
-            kern<<<g.nctas, PANEL_THREADS, smem, st>>>(op, M, x, partial);
-        };
-        switch (M.vbytes) {
-            case 1: run(k_panel<IT, SPLIT, uint8_t>); break;
-            case 2: run(k_panel<IT, SPLIT, uint16_t>); break;
-            default: run(k_panel<IT, SPLIT, uint32_t>); break;
-        }
+        const size_t smem = hc_offset<IT, SPLIT>(g) + panel_hc<SPLIT>() * sizeof(PanelTile);
+        if (SPLIT || !g.lazy) run_panel<IT, SPLIT, false>(op, M, x, partial, smem, st);
+        else run_panel<IT, SPLIT, !SPLIT>(op, M, x, partial, smem, st);
         count_launch();
         int e = (int)cudaGetLastError();
         if (e) return e;
     }
     if (op.rows) {
-        // each panel's row block is 16-byte aligned only if rows % VEC == 0
         constexpr int VEC = 16 / sizeof(IT);
-        const bool vec_ok = (op.rows % VEC) == 0;
-        const uint32_t work = vec_ok ? op.rows / VEC : op.rows;
+        const uint32_t work = (op.rows + VEC - 1) / VEC;
         const uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((work + 255) / 256, g.nctas * 8));
-        if (vec_ok)
-            k_panel_reduce<IT, VEC><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
-        else
-            k_panel_reduce<IT, 1><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, M, alpha, beta, y);
+        const bool y_aligned = ((uintptr_t)y & 15) == 0;
+        k_panel_reduce<IT><<<blocks, 256, 0, st>>>(partial, g.P, op.rows, g.rows_pad, M, alpha, beta, y,
+                                                   y_aligned);
         count_launch();
     }
     return (int)cudaGetLastError();

@@ -232,6 +232,49 @@ def test_overflow_adversarial(ff, oracle_mod, cuda):
                                                                   np.array([m - 1, m - 1]), 1, 1))
 
 
+@pytest.mark.parametrize("m", [251, 65521, 65536])
+def test_panel_overflow_adversarial(ff, oracle_mod, cuda, m):
+    """Panel tiles whose row sums approach 2^32: one dense row per section
+    kind (+1, -1 with x = 0, valued m-2 with x = m-1), long enough that the
+    lazy Barrett remainders (< 2m) would overflow a u32 and, for m = 65536,
+    that even exact residues would (the builder then keeps the rows layout)."""
+    for n, v, xv in ((65536, 1, m - 1), (65536, m - 1, 0), (40000, m - 2, m - 1),
+                     (65536, m - 2, m - 1)):
+        cols = n
+        ri = np.zeros(n, np.uint32)
+        ci = np.arange(n, dtype=np.uint32)
+        val = np.full(n, v, np.int64)
+        x = np.full(cols, xv, np.uint32)
+        A = ff.ffspmv_create(3, cols, ri, ci, val, m, strategy=2)
+        y0 = np.array([m - 1, 1, 0], np.uint32)
+        yd = dev(y0)
+        ff.ffspmv_apply(A, 1, dev(x), 1, yd)
+        assert np.array_equal(host(yd), oracle_mod.apply(3, cols, ri, ci, val, m, x, y0, 1, 1))
+
+
+@pytest.mark.parametrize("m", [3, 65521, 65537])
+def test_panel_pipeline_many_tiles(ff, oracle_mod, cuda, m):
+    """Panel schedule edge cases: > 64 tiles per CTA (header-cache reloads,
+    tiny 32 x 32 tiles) and tiles with more quads than the register ring
+    (> 16384 entries in one tile, the overflow loop)."""
+    g = synth.rng(77 + m % 1000)
+    for rows, cols, nnz, kw in ((6000, 6000, 60000, dict(panel_rows=32, panel_cols=32)),
+                                (20000, 20000, 120000, dict())):
+        ri, ci, val = synth.random_coo(g, rows, cols, nnz, m, dup=0.0, big=True)
+        A = ff.ffspmv_create(rows, cols, ri, ci, val, m, strategy=2, **kw)
+        assert A.info()["strategy_apply"] == ff.STRATEGY_PANELS
+        x = synth.uniform(g, cols, m)
+        y0 = synth.uniform(g, rows, m)
+        yd = dev(y0)
+        ff.ffspmv_apply(A, 7, dev(x), 3, yd)
+        assert np.array_equal(host(yd), oracle_mod.apply(rows, cols, ri, ci, val, m, x, y0, 7, 3))
+        xt = synth.uniform(g, rows, m)
+        ytd = dev(np.zeros(cols, np.uint32))
+        ff.ffspmv_apply_transpose(A, 1, dev(xt), 0, ytd)
+        assert np.array_equal(host(ytd), oracle_mod.apply_transpose(rows, cols, ri, ci, val, m, xt,
+                                                                    np.zeros(cols, np.uint32), 1, 0))
+
+
 def test_determinism_and_streams(ff, cuda):
     import torch
     m = 65521

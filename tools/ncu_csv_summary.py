@@ -62,3 +62,19 @@ if __name__ == "__main__":
         print(json.dumps(d, indent=1))
     if len(sys.argv) > 2:
         sass(sys.argv[2])
+
+
+def listing(path, counts):
+    """SASS lines whose execution count is in `counts` (in program order)."""
+    txt = open(path).read()
+    rows = list(csv.reader(io.StringIO(txt[txt.index('"Kernel Name"'):])))
+    hdr = rows[1]
+    iA, iE = hdr.index("Source"), hdr.index("Instructions Executed")
+    iS = hdr.index("Warp Stall Sampling (All Samples)")
+    for r in rows[2:]:
+        try:
+            n = int(r[iE])
+        except (ValueError, IndexError):
+            continue
+        if n in counts:
+            print(f"{n:8d} {r[iS]:>6s}  {r[iA].strip()}")
