@@ -134,8 +134,8 @@ struct BuildOptions {
 // the byte offset of its column in the staged x panel, (col - p*W) * xbytes,
 // in bits [rs, 32), and its band row, row - b*R, in bits [0, rs); rs = 14 /
 // 15 / 14 for x staged as u8 / u16 / u32 (W = 196608 / 65536 / 49152 columns
-// = 192 / 128 / 192 KB of shared memory, R = 8176 / 16320 / 4464 band rows of
-// u32 accumulators).  A tile writes one residue per band row into
+// = 192 / 128 / 192 KB of shared memory, R = 4088 / 8160 / 2200 band rows of
+// u32 accumulators, one band per thread group of the kernel, two groups).  A tile writes one residue per band row into
 // partial[p][row] (row stride rows_pad, a multiple of 16); a reduction pass
 // sums the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
 // spmv(y, Ai, x); reduce(y, m)").

@@ -25,14 +25,21 @@ void count_launch();
 namespace {
 
 constexpr int PANEL_THREADS = 1024;
+constexpr int PANEL_GT = 512;      // threads per group (two groups per CTA)
 
-// Shared memory: x panel (W * sizeof(IT)) | accumulators ((R + 1) u32, twice
-// when SPLIT) | tile-header cache (HC headers, 16-byte aligned).
+// Shared memory: x panel (W * sizeof(IT)) | accumulators of the two thread
+// groups (2 x (R + 1) u32, doubled when SPLIT) | tile-header cache (HC
+// headers, 16-byte aligned).
 template <bool SPLIT>
 __host__ __device__ constexpr uint32_t panel_hc() { return SPLIT ? 16u : 64u; }
+// u32 words per group accumulator block, a multiple of 4 (16-byte vectors)
+template <bool SPLIT>
+__host__ __device__ __forceinline__ uint32_t acc_stride(const PanelGeom &g) {
+    return ((SPLIT ? 2 : 1) * (g.R + 1) + 3) / 4 * 4;
+}
 template <class IT, bool SPLIT>
 __host__ __device__ __forceinline__ size_t hc_offset(const PanelGeom &g) {
-    return ((size_t)g.W * sizeof(IT) + (size_t)(g.R + 1) * 4 * (SPLIT ? 2 : 1) + 15) / 16 * 16;
+    return ((size_t)g.W * sizeof(IT) + 2 * (size_t)acc_stride<SPLIT>(g) * 4 + 15) / 16 * 16;
 }
 
 // Shared-memory accesses through 32-bit shared addresses (no generic-address
@@ -108,6 +115,22 @@ __device__ __forceinline__ void vals(const uint4 &v, uint32_t (&a)[4]) {
     } else {
         a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
     }
+}
+
+// Bulk L2 prefetch of a tile's quads and value quads (16-byte granules).
+__device__ __forceinline__ void prefetch_l2(const void *p, uint64_t bytes) {
+    const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15, e = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+    for (uintptr_t q = a; q < e; q += 1u << 20) {
+        const uint32_t n = (uint32_t)min((uintptr_t)(1u << 20), e - q);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(n) : "memory");
+    }
+}
+template <class IT>
+__device__ __forceinline__ void prefetch_tile(const DevPanel &op, const PanelTile &T) {
+    const uint32_t nq = T.nqp + T.nqm + T.nqv;
+    if (nq) prefetch_l2(reinterpret_cast<const uint4 *>(op.pent) + T.q0, 16ull * nq);
+    if (T.nqv) prefetch_l2(reinterpret_cast<const unsigned char *>(op.vval) + 4ull * sizeof(IT) * T.vq0,
+                           4ull * sizeof(IT) * T.nqv);
 }
 
 // x panel -> shared memory, converted to the narrow staged type.  Eight
@@ -200,70 +223,74 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict_
     extern __shared__ __align__(16) unsigned char smem[];
     const PanelGeom g = op.g;
     IT *sx = reinterpret_cast<IT *>(smem);
-    uint32_t *acc = reinterpret_cast<uint32_t *>(smem + (size_t)g.W * sizeof(IT));
+    const uint32_t tid = threadIdx.x, grp = tid / PANEL_GT, gt = tid % PANEL_GT;
+    // each thread group has its own band accumulators (R + 1 u32, twice when
+    // SPLIT: the high halves follow the low ones)
+    constexpr uint32_t AW = SPLIT ? 2 : 1;
+    uint32_t *acc = reinterpret_cast<uint32_t *>(smem + (size_t)g.W * sizeof(IT)) + grp * acc_stride<SPLIT>(g);
     const uint32_t sx_s = (uint32_t)__cvta_generic_to_shared(sx);
     const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);
-    const uint32_t hi_off = 4 * (g.R + 1);           // SPLIT: high halves after the low ones
+    const uint32_t hi_off = 4 * (g.R + 1);
     const uint32_t rs = g.rs, rmask = (1u << g.rs) - 1, dummy = g.R;
     const uint32_t t0 = op.cta_t0[blockIdx.x], t1 = op.cta_t0[blockIdx.x + 1];
     const uint4 *pq = reinterpret_cast<const uint4 *>(op.pent);
-    const uint32_t tid = threadIdx.x;
     constexpr uint32_t HC = panel_hc<SPLIT>();
-    for (uint32_t i = tid; i < (g.R + 1) * (SPLIT ? 2 : 1); i += PANEL_THREADS) acc[i] = 0;
-    uint32_t cur_p = 0xFFFFFFFFu;
-    // Software pipeline over the CTA's tiles: the headers sit in shared
-    // memory, and the first QR quads per thread of tile t+1 (the
-    // whole tile when it has <= QR * 1024 quads) are loaded into registers
-    // before tile t's write-out, so the stream latency hides behind it.
+    for (uint32_t i = gt; i < AW * (g.R + 1); i += PANEL_GT) acc[i] = 0;
+    auto bar_group = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(PANEL_GT)); };
+    // Software pipeline over a group's tiles: the first QR quads per thread
+    // of its next tile (the whole tile when it has <= QR * PANEL_GT quads)
+    // are loaded into registers before the current tile's write-out, so the
+    // stream latency hides behind it.
     constexpr int QR = SPLIT ? 2 : 4;
     uint4 rw[QR], ra[QR];
     auto load_regs = [&](const PanelTile &T) {
         const uint32_t nq = T.nqp + T.nqm + T.nqv, ev = T.nqp + T.nqm;
 #pragma unroll
         for (int i = 0; i < QR; ++i) {
-            const uint32_t q = tid + i * PANEL_THREADS;
+            const uint32_t q = gt + i * PANEL_GT;
             if (q < nq) {
                 rw[i] = ld_quad(pq + T.q0 + q, true, dummy);
                 ra[i] = ld_vraw<IT>(op.vval, (uint64_t)T.vq0 + (q - ev), q >= ev);
             }
         }
     };
-    // tile headers of the CTA's range, HC at a time, in shared memory
     PanelTile *hc = reinterpret_cast<PanelTile *>(smem + hc_offset<IT, SPLIT>(g));
-    auto fill_hc = [&](uint32_t tb) {
-        for (uint32_t i = tid; i < 2 * HC; i += PANEL_THREADS)
-            if (tb + i / 2 < t1)
-                reinterpret_cast<uint4 *>(hc)[i] = __ldg(reinterpret_cast<const uint4 *>(op.tiles + tb) + i);
-    };
-    // the current header is read from shared memory where it is used (no
-    // registers held across the tile)
-    uint32_t jc = 0;
-    if (t0 < t1) {
-        fill_hc(t0);
-        __syncthreads();
-        load_regs(hc[0]);
-    }
-    for (uint32_t t = t0; t < t1; ++t) {
-        const PanelTile &T = hc[jc];
-        if (T.p != cur_p) {
-            const uint64_t c0 = (uint64_t)T.p * g.W;
+    // Segments: runs of the CTA's tiles with one x panel and at most HC
+    // tiles.  A segment stages its panel and headers with the whole CTA; then
+    // group 0 takes its even tiles and group 1 its odd tiles, each group
+    // synchronising only its own 16 warps, so one group's write-out overlaps
+    // the other's accumulation.
+    for (uint32_t s0 = t0; s0 < t1;) {
+        __syncthreads();                       // previous segment done with x and hc
+        const uint32_t cnt = min(HC, t1 - s0);
+        for (uint32_t i = tid; i < 2 * cnt; i += PANEL_THREADS)
+            reinterpret_cast<uint4 *>(hc)[i] = __ldg(reinterpret_cast<const uint4 *>(op.tiles + s0) + i);
+        const uint32_t p = __ldg(&op.tiles[s0].p);
+        {
+            const uint64_t c0 = (uint64_t)p * g.W;
             const uint32_t wn = (uint32_t)min((uint64_t)g.W, (uint64_t)op.cols - c0);
             stage_x<IT>(sx, xin, c0, wn);
-            cur_p = T.p;
         }
         __syncthreads();
-        {
+        uint32_t n = 1;
+        while (n < cnt && hc[n].p == p) ++n;
+        if (grp < n) load_regs(hc[grp]);
+        if (gt == 0 && grp + 2 < n) prefetch_tile<IT>(op, hc[grp + 2]);
+        for (uint32_t j = grp; j < n; j += 2) {
+            const PanelTile &T = hc[j];
+            // the group's tile after next -> L2, so its register loads hit L2
+            if (gt == 0 && j + 4 < n) prefetch_tile<IT>(op, hc[j + 4]);
             const uint32_t e1 = T.nqp, e2 = T.nqp + T.nqm, nq = e2 + T.nqv;
 #pragma unroll
             for (int i = 0; i < QR; ++i) {
-                const uint32_t q = tid + i * PANEL_THREADS;
+                const uint32_t q = gt + i * PANEL_GT;
                 if (q < nq)
                     do_quad<IT, SPLIT, LAZY>(q < e1 ? 0u : q < e2 ? 1u : 2u, rw[i], ra[i], sx_s, acc_s,
                                              hi_off, rs, rmask, M);
             }
             // quads beyond the register ring: two per thread per round
-            for (uint32_t q = tid + QR * PANEL_THREADS; q < nq; q += 2 * PANEL_THREADS) {
-                const uint32_t qb = q + PANEL_THREADS;
+            for (uint32_t q = gt + QR * PANEL_GT; q < nq; q += 2 * PANEL_GT) {
+                const uint32_t qb = q + PANEL_GT;
                 const uint4 w0 = ld_quad(pq + T.q0 + q, true, dummy);
                 const uint4 w1 = ld_quad(pq + T.q0 + qb, qb < nq, dummy);
                 const uint4 a0 = ld_vraw<IT>(op.vval, (uint64_t)T.vq0 + (q - e2), q >= e2);
@@ -273,62 +300,56 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict_
                     do_quad<IT, SPLIT, LAZY>(qb < e1 ? 0u : qb < e2 ? 1u : 2u, w1, a1, sx_s, acc_s, hi_off, rs,
                                              rmask, M);
             }
-        }
-        // read before the barrier: after it, fill_hc may overwrite the cache
-        const uint32_t p = T.p, b = T.b, rn = T.rn;
-        __syncthreads();
-        if (t + 1 < t1) {
-            const uint32_t j = (t + 1 - t0) % HC;
-            if (j == 0) {            // next chunk of headers (uniform branch)
-                fill_hc(t + 1);
-                __syncthreads();
-            }
-            jc = j;
-            load_regs(hc[j]);
-        }
-        // one residue per band row -> partial[p][row] (same narrow type as the
-        // staged x); re-zero the accumulators.  Four rows per thread per step:
-        // one conflict-free 16-byte shared load (lanes read consecutive
-        // vectors) and one 4 * sizeof(IT)-byte store.  Without SPLIT the row
-        // sum is < 2^32 (checked by the builder) and reduces with the 32-bit
-        // Barrett; SPLIT: the residue of lo + hi * 2^16.  Rows rn ..
-        // round16(rn) hold zeros (no entries) and land in the padding.
-        IT *out = partial + (uint64_t)p * g.rows_pad + (uint64_t)b * g.R;
-        const uint32_t nv = (rn + 3) / 4;
-        for (uint32_t v = tid; v < nv; v += PANEL_THREADS) {
-            const uint4 s4 = reinterpret_cast<const uint4 *>(acc)[v];
-            reinterpret_cast<uint4 *>(acc)[v] = make_uint4(0, 0, 0, 0);
-            uint32_t res[4];
-            if constexpr (SPLIT) {
-                const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+            const uint32_t b = T.b, rn = T.rn;
+            bar_group();                       // the tile's sums are complete
+            if (j + 2 < n) load_regs(hc[j + 2]);
+            // one residue per band row -> partial[p][row] (same narrow type
+            // as the staged x); re-zero the accumulators.  Four rows per
+            // thread per step: one conflict-free 16-byte shared load (lanes
+            // read consecutive vectors) and one 4 * sizeof(IT)-byte store.
+            // Without SPLIT the row sum is < 2^32 (checked by the builder)
+            // and reduces with the 32-bit Barrett; SPLIT: the residue of lo +
+            // hi * 2^16.  Rows rn .. round4(rn) hold zeros and land in the
+            // padding of the last band.
+            IT *out = partial + (uint64_t)p * g.rows_pad + (uint64_t)b * g.R;
+            const uint32_t nv = (rn + 3) / 4;
+            for (uint32_t v = gt; v < nv; v += PANEL_GT) {
+                const uint4 s4 = reinterpret_cast<const uint4 *>(acc)[v];
+                reinterpret_cast<uint4 *>(acc)[v] = make_uint4(0, 0, 0, 0);
+                uint32_t res[4];
+                if constexpr (SPLIT) {
+                    const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t r = 4 * v + i;
-                    res[i] = mod64((uint64_t)sv[i] + ((uint64_t)acc[g.R + 1 + r] << 16), M);
-                    acc[g.R + 1 + r] = 0;
-                }
-                asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(
-                                 reinterpret_cast<uint4 *>(out) + v),
-                             "r"(res[0]), "r"(res[1]), "r"(res[2]), "r"(res[3]), "l"(POLICY_EVICT_LAST));
-            } else {
-                res[0] = mod32_min(s4.x, M);
-                res[1] = mod32_min(s4.y, M);
-                res[2] = mod32_min(s4.z, M);
-                res[3] = mod32_min(s4.w, M);
-                if constexpr (sizeof(IT) == 1) {
-                    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(
-                                     reinterpret_cast<uint32_t *>(out) + v),
-                                 "r"(__byte_perm(__byte_perm(res[0], res[1], 0x0040), __byte_perm(res[2], res[3], 0x0040), 0x5410)),
-                                 "l"(POLICY_EVICT_LAST));
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t r = 4 * v + i;
+                        res[i] = mod64((uint64_t)sv[i] + ((uint64_t)acc[g.R + 1 + r] << 16), M);
+                        acc[g.R + 1 + r] = 0;
+                    }
+                    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(
+                                     reinterpret_cast<uint4 *>(out) + v),
+                                 "r"(res[0]), "r"(res[1]), "r"(res[2]), "r"(res[3]), "l"(POLICY_EVICT_LAST));
                 } else {
-                    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(
-                                     reinterpret_cast<uint2 *>(out) + v),
-                                 "r"(__byte_perm(res[0], res[1], 0x5410)), "r"(__byte_perm(res[2], res[3], 0x5410)),
-                                 "l"(POLICY_EVICT_LAST));
+                    res[0] = mod32_min(s4.x, M);
+                    res[1] = mod32_min(s4.y, M);
+                    res[2] = mod32_min(s4.z, M);
+                    res[3] = mod32_min(s4.w, M);
+                    if constexpr (sizeof(IT) == 1) {
+                        asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(
+                                         reinterpret_cast<uint32_t *>(out) + v),
+                                     "r"(__byte_perm(__byte_perm(res[0], res[1], 0x0040),
+                                                     __byte_perm(res[2], res[3], 0x0040), 0x5410)),
+                                     "l"(POLICY_EVICT_LAST));
+                    } else {
+                        asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(
+                                         reinterpret_cast<uint2 *>(out) + v),
+                                     "r"(__byte_perm(res[0], res[1], 0x5410)), "r"(__byte_perm(res[2], res[3], 0x5410)),
+                                     "l"(POLICY_EVICT_LAST));
+                    }
                 }
             }
+            bar_group();                       // zeroing done before the next tile adds
         }
-        // the next tile's __syncthreads orders these writes before reuse
+        s0 += n;
     }
 }
 
@@ -345,7 +366,21 @@ __global__ void k_panel_reduce(const IT *__restrict__ partial, uint32_t P, uint3
         uint64_t s[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) s[i] = 0;
-        for (uint32_t p = 0; p < P; ++p) {   // P residues < 2^32: exact in u64
+        // P residues < 2^32: exact in u64; four panels' loads in flight
+        uint32_t p = 0;
+        for (; p + 4 <= P; p += 4) {
+            uint4 e4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                e4[j] = __ldcs(reinterpret_cast<const uint4 *>(partial + (uint64_t)(p + j) * rows_pad) + v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const IT *e = reinterpret_cast<const IT *>(&e4[j]);
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) s[i] += e[i];
+            }
+        }
+        for (; p < P; ++p) {
             const uint4 e4 = __ldcs(reinterpret_cast<const uint4 *>(partial + (uint64_t)p * rows_pad) + v);
             const IT *e = reinterpret_cast<const IT *>(&e4);
 #pragma unroll

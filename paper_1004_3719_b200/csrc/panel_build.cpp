@@ -14,12 +14,13 @@ PanelGeom panel_geometry(uint64_t rows, uint64_t cols, uint32_t m, const BuildOp
     // staged x element = narrowest type holding a residue
     g.xbytes = m <= 256u ? 1 : m <= 65536u ? 2 : 4;
     g.split = m > 65536u ? 1 : 0;
-    // smem: W * xbytes (x panel) + (R + 1) * 4 * (1 + split) (accumulators + the
-    // dummy row) + the tile-header cache (PANEL_HC) <= 227 KB.  Packed word: byte offset (< W * xbytes) above rs
+    // smem: W * xbytes (x panel) + 2 * (R + 1) * 4 * (1 + split) (the
+    // accumulators + dummy row of the kernel's two thread groups) + the
+    // tile-header cache (PANEL_HC) <= 227 KB.  Packed word: byte offset (< W * xbytes) above rs
     // row bits, R < 2^rs.
-    if (g.xbytes == 1) { g.W = 196608u; g.rs = 14; g.R = 8176u; }
-    else if (g.xbytes == 2) { g.W = 65536u; g.rs = 15; g.R = 16320u; }
-    else { g.W = 49152u; g.rs = 14; g.R = 4400u; }
+    if (g.xbytes == 1) { g.W = 196608u; g.rs = 14; g.R = 4088u; }
+    else if (g.xbytes == 2) { g.W = 65536u; g.rs = 15; g.R = 8160u; }
+    else { g.W = 49152u; g.rs = 14; g.R = 2200u; }
     if (bo.panel_cols) g.W = std::min<uint32_t>(bo.panel_cols, g.W);
     if (bo.panel_rows) g.R = std::min<uint32_t>(bo.panel_rows, g.R);
     g.P = (uint32_t)((cols + g.W - 1) / g.W);

@@ -144,7 +144,7 @@ def test_panel_strategy_choice(lib):
     info = lib.ffspmv_analyze(M["rows"], M["cols"], M["row"], M["col"], M["val"], M["m"])
     assert info["gather_locality"] > 0.7
     assert info["strategy_apply"] == lib.STRATEGY_PANELS == info["strategy_transpose"]
-    assert info["panels"] == 8 and info["panel_bands"] == -(-M["rows"] // 16320)
+    assert info["panels"] == 8 and info["panel_bands"] == -(-M["rows"] // 8160)
     # banded matrix: columns local -> rows layout
     n = 1 << 19
     ri = np.repeat(np.arange(n, dtype=np.uint32), 4)
