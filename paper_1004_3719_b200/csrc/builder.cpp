@@ -34,7 +34,7 @@ DevMod make_mod(uint32_t m) {
     d.mu = (uint64_t)(two64 / m);
     d.r64 = (uint64_t)(two64 % m);
     d.mu32 = (uint32_t)std::min<uint64_t>((1ull << 32) / m, 0xFFFFFFFFull);
-    d.pad_ = 0;
+    d.r32 = (uint32_t)((1ull << 32) % m);
     return d;
 }
 

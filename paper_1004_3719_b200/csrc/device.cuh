@@ -70,6 +70,18 @@ __device__ __forceinline__ uint32_t mod32(uint32_t x, const DevMod &M) {
     uint32_t r = x - __umulhi(x, M.mu32) * M.m;
     return r >= M.m ? r - M.m : r;
 }
+// x mod m for x < 2^32, m <= 2^16: Barrett remainder r in [0, 2m), then
+// min(r, r - m) as unsigned (r - m wraps to a huge value when r < m).
+__device__ __forceinline__ uint32_t mod32_min(uint32_t x, const DevMod &M) {
+    const uint32_t r = __umulhi(x, M.mu32) * (0u - M.m) + x;
+    return min(r, r - M.m);
+}
+// s mod m for s < 2^48, m <= 2^16: s = h 2^32 + l with h < 2^16, so
+// h (2^32 mod m) < 2^32; both halves reduce with mod32_min.
+__device__ __forceinline__ uint32_t mod48(uint64_t s, const DevMod &M) {
+    const uint32_t u = mod32_min((uint32_t)s, M) + mod32_min((uint32_t)(s >> 32) * M.r32, M);
+    return min(u, u - M.m);
+}
 // (hi * 2^64 + lo) mod m, hi < 2^32: hi mod m < m, (hi mod m)*(2^64 mod m) +
 // (lo mod m) < m^2 + m < 2^64.
 __device__ __forceinline__ uint32_t mod96(uint32_t hi, uint64_t lo, const DevMod &M) {

@@ -69,7 +69,7 @@ struct DevMod {
     uint64_t mu;         // floor(2^64 / m)
     uint64_t r64;        // 2^64 mod m
     uint32_t mu32;       // floor(2^32 / m) (used when m <= 2^16)
-    uint32_t pad_;
+    uint32_t r32;        // 2^32 mod m
 };
 
 // Device view of one packed operator (A or A^T).
@@ -135,8 +135,8 @@ struct BuildOptions {
 // in bits [rs, 32), and its band row, row - b*R, in bits [0, rs); rs = 14 /
 // 15 / 14 for x staged as u8 / u16 / u32 (W = 196608 / 65536 / 49152 columns
 // = 192 / 128 / 192 KB of shared memory, R = 4088 / 8160 / 2200 band rows of
-// u32 accumulators, one band per thread group of the kernel, two groups).  A tile writes one residue per band row into
-// partial[p][row] (row stride rows_pad, a multiple of 16); a reduction pass
+// u32 accumulators, one band per thread group of the kernel, two groups).  A
+// tile writes one residue per band row into partial[p][row] (row stride rows_pad, a multiple of 16); a reduction pass
 // sums the P partials of each row (Fig. 2 "foreach submatrix Ai in A do
 // spmv(y, Ai, x); reduce(y, m)").
 struct Canon;

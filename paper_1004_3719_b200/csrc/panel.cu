@@ -173,13 +173,6 @@ __device__ __forceinline__ void stage_x(IT *sx, const uint32_t *__restrict__ x, 
     for (uint32_t i = done + threadIdx.x; i < wn; i += PANEL_THREADS) sx[i] = (IT)__ldg(src + i);
 }
 
-// x mod m for x < 2^32, m <= 2^16: Barrett remainder r in [0, 2m), then
-// min(r, r - m) as unsigned (r - m wraps to a huge value when r < m).
-__device__ __forceinline__ uint32_t mod32_min(uint32_t x, const DevMod &M) {
-    const uint32_t r = __umulhi(x, M.mu32) * (0u - M.m) + x;
-    return min(r, r - M.m);
-}
-
 // (a * x) mod m of a valued entry.  LAZY: the Barrett remainder before its
 // correction, in [0, 2m) (mod32's argument; the builder checked that a tile
 // row's sum of such terms stays < 2^32).

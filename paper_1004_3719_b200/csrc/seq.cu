@@ -210,6 +210,7 @@ struct SeqLayout {
     IT *Uc;          // n x ku (unfused path) or n x KUP padded (fused path)
     uint32_t *partial[2];
     uint32_t *ufrag; // tensor-core path: per slice 256 u32 of U limbs in fragment order
+    DevOp *opdev;    // device copy of the operator view (out-of-line scalar path)
     size_t bytes;
 };
 
@@ -240,6 +241,7 @@ SeqLayout<IT> layout(void *ws, const DevOp &op, uint32_t m, uint32_t k, uint32_t
     L.partial[0] = (uint32_t *)(p + off); off += pb;
     L.partial[1] = (uint32_t *)(p + off); off += pb;
     L.ufrag = (uint32_t *)(p + off); off += fb;
+    L.opdev = (DevOp *)(p + off); off += align256(sizeof(DevOp));
     L.bytes = off;
     return L;
 }
@@ -339,10 +341,34 @@ int launch_step_mma_t(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku,
     return (int)cudaGetLastError();
 }
 
+template <class VT, int LPR>
+int launch_step_h_t(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
+                    const uint16_t *Vin, uint16_t *Vout, const uint32_t *U, const uint32_t *ufrag,
+                    uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc,
+                    cudaStream_t st) {
+    auto kern = k_seq_step_h<VT, LPR>;
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SMMA_WARPS * 32, 0);
+        occ = std::max(1, std::min<int>(occ, (int)MAX_STEP_CTAS_PER_SM));
+    }
+    const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    const uint32_t nctas = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)num_sms() * occ, (items + SMMA_WARPS - 1) / SMMA_WARPS));
+    kern<<<nctas, SMMA_WARPS * 32, 0, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp);
+    count_launch();
+    nc = nctas;
+    return (int)cudaGetLastError();
+}
+
 template <class VT>
-int launch_step_mma(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku, const uint16_t *Vin,
-                    uint16_t *Vout, const uint32_t *U, const uint32_t *ufrag, uint32_t *po,
-                    const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc, cudaStream_t st) {
+int launch_step_mma(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
+                    const uint16_t *Vin, uint16_t *Vout, const uint32_t *U, const uint32_t *ufrag,
+                    uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc,
+                    cudaStream_t st) {
+    // k = 8 / 16: the lean half-slice kernel (16-byte gathers, one row per lane)
+    if (k == 8) return launch_step_h_t<VT, 1>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+    if (k == 16) return launch_step_h_t<VT, 2>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
     if (k <= 4) return launch_step_mma_t<VT, 1, 4>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
     if (k <= 8) return launch_step_mma_t<VT, 2, 8>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
     return launch_step_mma_t<VT, 4, 16>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
@@ -355,6 +381,7 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
     const uint32_t *Uu = U ? U : X;
     const uint32_t pairs = ku * k;
     int err;
+    if ((err = (int)cudaMemcpyAsync(W.opdev, &op, sizeof(DevOp), cudaMemcpyHostToDevice, st))) return err;
     {
         uint64_t tot = n * (uint64_t)k;
         uint32_t blocks = (uint32_t)std::min<uint64_t>((tot + 255) / 256, (uint64_t)num_sms() * 8);
@@ -379,8 +406,8 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
         const uint32_t *pp = W.partial[(t - 1) & 1];
         uint32_t *Sp = S + (t - 1) * pairs;
         err = M.vbytes == 1
-                  ? launch_step_mma<uint8_t>(op, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st)
-                  : launch_step_mma<uint16_t>(op, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
+                  ? launch_step_mma<uint8_t>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st)
+                  : launch_step_mma<uint16_t>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
         if (err) return err;
         nprev = nc;
     }

@@ -287,4 +287,210 @@ k_seq_step_mma(DevOp op, DevMod M, uint32_t k, uint32_t ku, const uint16_t *__re
     }
 }
 
+// ------------------------------------------------ lean half-slice variant --
+// k in {8, 16}: LPR = k / 8 lanes per row, each lane owns one row and 8
+// iterate columns (one 16-byte gather per nonzero), and a warp walks a 32-row
+// slice in LPR passes of 32 / LPR rows.  Per lane: 8 u32 accumulators for the
+// +-1 part (a -1 adds m - x: < 2^32 for the <= 512 entries of a slice row)
+// and 8 u64 accumulators for the valued part (products < 2^32).  The gathers
+// of slot j+1 are issued before slot j is accumulated, and the index words
+// are read two slots ahead.  ~60 registers -> 4 CTAs of 8 warps per SM.
+__device__ __forceinline__ uint4 gather16(const uint16_t *__restrict__ V, uint32_t word, uint32_t k,
+                                          uint32_t c0) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    const uint16_t *p = V + (uint64_t)(word & COL_MASK) * k + c0;
+    asm volatile("{.reg .pred q; setp.ne.u32 q, %5, %6;\n"
+                 "@q ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];}"
+                 : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+                 : "l"(p), "r"(word), "r"(PAD_COL));
+    return v;
+}
+
+template <class VT, int LPR>
+__device__ __forceinline__ void seq_slice_h(const DevOp &op, const DevMod &M, uint32_t s,
+                                            const SliceHdr &h, uint32_t lane, uint32_t k,
+                                            const uint16_t *__restrict__ Vin,
+                                            uint16_t *__restrict__ Vout,
+                                            const uint32_t *__restrict__ ufrag, uint8_t *vt,
+                                            unsigned long long *p64) {
+    constexpr uint32_t RPP = 32 / LPR;
+    const uint32_t m = M.m, wp = h.wp, wv = h.wv;
+    const uint32_t c0 = (lane % LPR) * 8;
+    const uint32_t *pc = op.pcol + h.off_p + lane;
+    const uint32_t *vc = op.vcol + h.off_v + lane;
+    const VT *vv = reinterpret_cast<const VT *>(op.vval) + h.off_v + lane;
+#pragma unroll
+    for (uint32_t pass = 0; pass < (uint32_t)LPR; ++pass) {
+        const uint32_t rl = pass * RPP + lane / LPR;
+        uint32_t a32[8];
+        unsigned long long a64[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { a32[i] = 0; a64[i] = 0; }
+        // +-1 slots: x, or m - x for a -1 (sign bit of the index word)
+        {
+            uint32_t w1 = wp > 1 ? ld_bcast(pc + 32) : PAD_COL;
+            uint32_t c = __shfl_sync(0xFFFFFFFFu, wp ? ld_bcast(pc) : PAD_COL, rl);
+            uint4 x = gather16(Vin, c, k, c0);
+            for (uint32_t j = 0; j < wp; ++j) {
+                const uint32_t w2 = j + 2 < wp ? ld_bcast(pc + (j + 2) * 32) : PAD_COL;
+                const uint32_t cn = __shfl_sync(0xFFFFFFFFu, w1, rl);
+                const uint4 xn = gather16(Vin, cn, k, c0);
+                // -1: (v ^ ~0) + (m + 1) = m - v  (mod 2^32)
+                const uint32_t sm = (c & SIGN_BIT) && c != PAD_COL ? 0xFFFFFFFFu : 0u, sa = sm & (m + 1);
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    a32[2 * i] += ((xs[i] & 0xFFFFu) ^ sm) + sa;
+                    a32[2 * i + 1] += ((xs[i] >> 16) ^ sm) + sa;
+                }
+                c = cn;
+                x = xn;
+                w1 = w2;
+            }
+        }
+        // valued slots
+        {
+            uint32_t w1 = wv > 1 ? ld_bcast(vc + 32) : PAD_COL;
+            uint32_t v1 = wv > 1 ? ld_bcast(vv + 32) : 0u;
+            uint32_t c = __shfl_sync(0xFFFFFFFFu, wv ? ld_bcast(vc) : PAD_COL, rl);
+            uint32_t a = __shfl_sync(0xFFFFFFFFu, wv ? ld_bcast(vv) : 0u, rl);
+            uint4 x = gather16(Vin, c, k, c0);
+            for (uint32_t j = 0; j < wv; ++j) {
+                const uint32_t w2 = j + 2 < wv ? ld_bcast(vc + (j + 2) * 32) : PAD_COL;
+                const uint32_t v2 = j + 2 < wv ? ld_bcast(vv + (j + 2) * 32) : 0u;
+                const uint32_t cn = __shfl_sync(0xFFFFFFFFu, w1, rl);
+                const uint32_t an = __shfl_sync(0xFFFFFFFFu, v1, rl);
+                const uint4 xn = gather16(Vin, cn, k, c0);
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    a64[2 * i] += (unsigned long long)a * (xs[i] & 0xFFFFu);
+                    a64[2 * i + 1] += (unsigned long long)a * (xs[i] >> 16);
+                }
+                c = cn;
+                a = an;
+                x = xn;
+                w1 = w2;
+                v1 = v2;
+            }
+        }
+        // residues -> V_{t+1} (one 16-byte store) and the transposed limb
+        // tile VT[plane][col][row] (bytes) for the projection
+        // row sums < 512 (2^32 + 2^16) < 2^48 (slice rows hold <= long_row <=
+        // 65535 entries: < 2^48 as well)
+        uint32_t r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = mod48(a64[i] + a32[i], M);
+        if (rl >= h.nrows) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = 0;
+        } else if (c0 < k) {
+            const uint32_t row = op.perm[s * 32 + rl];
+            *reinterpret_cast<uint4 *>(Vout + (uint64_t)row * k + c0) =
+                make_uint4(r[0] | r[1] << 16, r[2] | r[3] << 16, r[4] | r[5] << 16, r[6] | r[7] << 16);
+        }
+        if (c0 < k) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                vt[(c0 + i) * 32 + rl] = (uint8_t)(r[i] >> 8);
+                vt[32 * 32 + (c0 + i) * 32 + rl] = (uint8_t)r[i];
+            }
+        }
+    }
+    __syncwarp();
+    // projection of the slice: U^T V as in seq_slice_mma
+    const uint4 ah4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256) + lane);
+    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
+    const uint32_t ah[4] = {ah4.x, ah4.y, ah4.z, ah4.w}, al[4] = {al4.x, al4.y, al4.z, al4.w};
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < LPR; ++nt) {
+        const uint32_t b = nt * 8 + gid;
+        uint32_t bh[2], bl[2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const uint32_t off = b * 32 + tig * 4 + 16 * jj;
+            bh[jj] = *reinterpret_cast<const uint32_t *>(vt + off);
+            bl[jj] = *reinterpret_cast<const uint32_t *>(vt + 32 * 32 + off);
+        }
+        int hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
+        mma_u8(hh, ah, bh);
+        mma_u8(cr, ah, bl);
+        mma_u8(cr, al, bh);
+        mma_u8(ll, al, bl);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            p64[(nt * 4 + e) * 32 + lane] += ((unsigned long long)(uint32_t)hh[e] << 16) +
+                                             ((unsigned long long)(uint32_t)cr[e] << 8) +
+                                             (uint32_t)ll[e];
+    }
+    __syncwarp();
+}
+
+// rows outside SELL slices (long rows, CSR / COO_S groups, zero rows): kept
+// out of line so their register needs do not constrain the slice path
+// (reads the operator view from a device copy: taking the address of the
+// kernel parameter would move it to local memory for the whole kernel)
+template <class VT, int KP>
+__device__ __noinline__ void seq_item_scalar(const DevOp *__restrict__ opg, const DevMod M, uint32_t w,
+                                             uint32_t lane, uint32_t k, const uint16_t *__restrict__ Vin,
+                                             SeqScalarOut o) {
+    const DevOp op = *opg;
+    block_item<VT, KP, 8>(op, M, w, lane, k, Vin, k, o);
+}
+
+template <class VT, int LPR>
+__global__ void __launch_bounds__(SMMA_WARPS * 32, 3)
+k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, uint32_t ku,
+             const uint16_t *__restrict__ Vin,
+             uint16_t *__restrict__ Vout, const uint32_t *__restrict__ U,
+             const uint32_t *__restrict__ ufrag, uint32_t *__restrict__ part_out,
+             const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev) {
+    __shared__ __align__(16) uint8_t vts[SMMA_WARPS][2 * 32 * 32];
+    __shared__ unsigned long long pn[16 * SMMA_KMAX];
+    __shared__ unsigned long long p64s[SMMA_WARPS][SMMA_P64];
+    __shared__ uint32_t red[SMMA_WARPS][16][SMMA_KMAX];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
+    const uint32_t pairs = ku * k;
+    for (uint32_t i = threadIdx.x; i < 16 * SMMA_KMAX; i += SMMA_WARPS * 32) pn[i] = 0;
+    for (uint32_t i = lane; i < SMMA_P64; i += 32) p64s[warp][i] = 0;
+    __syncthreads();
+    for (uint32_t p = gw; part_prev && p < pairs; p += nw) {
+        uint64_t sacc = 0;
+        for (uint32_t c = lane; c < nprev; c += 32) sacc += part_prev[(uint64_t)c * pairs + p];
+        for (int o = 16; o; o >>= 1) sacc += __shfl_xor_sync(0xFFFFFFFFu, sacc, o);
+        if (lane == 0) S_prev[p] = mod64(sacc, M);
+    }
+    unsigned long long *p64 = p64s[warp];
+    SeqScalarOut sout{Vout, U, k, ku, pn};
+    const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    for (uint32_t w = gw; w < items; w += nw) {
+        if (w >= op.n_long && w - op.n_long < op.n_slices) {
+            const uint32_t s = w - op.n_long;
+            const SliceHdr h = load_hdr_b(op.slices + s);
+            seq_slice_h<VT, LPR>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], p64);
+        } else {
+            seq_item_scalar<VT, 8 * LPR>(opdev, M, w, lane, k, Vin, sout);
+        }
+    }
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < LPR; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t a = gid + 8 * (e >> 1), b = nt * 8 + tig * 2 + (e & 1);
+            red[warp][a][b] = mod64(p64[(nt * 4 + e) * 32 + lane], M);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < pairs; i += SMMA_WARPS * 32) {
+        const uint32_t a = i / k, b = i - a * k;
+        uint64_t sacc = mod64(pn[a * k + b], M);
+#pragma unroll
+        for (int w = 0; w < SMMA_WARPS; ++w) sacc += red[w][a][b];
+        part_out[(uint64_t)blockIdx.x * pairs + i] = mod64(sacc, M);
+    }
+}
+
 }  // namespace ffspmv
