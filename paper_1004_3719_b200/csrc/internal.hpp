@@ -13,6 +13,8 @@ namespace ffspmv {
 // A slot whose column is PAD_COL contributes nothing (ELL padding).
 // Valid columns are < 2^31 - 1, so the sentinel never collides.
 constexpr uint32_t PAD_COL = 0x7FFFFFFFu;
+// dynamic shared memory a k_panel CTA may use (227 KB opt-in maximum)
+constexpr uint64_t PANEL_SMEM_MAX = 232448;
 // Bit 31 of an index-only (+-1) slot is the sign: set = "-1".
 constexpr uint32_t SIGN_BIT = 0x80000000u;
 constexpr uint32_t COL_MASK = 0x7FFFFFFFu;

@@ -173,6 +173,14 @@ __device__ __forceinline__ void stage_x(IT *sx, const uint32_t *__restrict__ x, 
     for (uint32_t i = done + threadIdx.x; i < wn; i += PANEL_THREADS) sx[i] = (IT)__ldg(src + i);
 }
 
+// a * b + c (mod 2^32) kept as one IMAD (the compiler otherwise rewrites
+// q * (0 - m) + x as a negation plus a multiply-add)
+__device__ __forceinline__ uint32_t mad32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 // (a * x) mod m of a valued entry.  LAZY: the Barrett remainder before its
 // correction, in [0, 2m) (mod32's argument; the builder checked that a tile
 // row's sum of such terms stays < 2^32).
@@ -181,7 +189,7 @@ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t xv, const DevMod
     if constexpr (SPLIT) return mod64((uint64_t)a * xv, M);
     else if constexpr (LAZY) {
         const uint32_t p = a * xv;
-        return __umulhi(p, M.mu32) * (0u - M.m) + p;
+        return mad32(__umulhi(p, M.mu32), 0u - M.m, p);
     } else return mod32(a * xv, M);
 }
 
@@ -210,6 +218,12 @@ __device__ __forceinline__ void do_quad(uint32_t kind, const uint4 &w, const uin
     }
 }
 
+// x mod m for x < 2^32, m <= 2^16 (mod32_min with the multiply-add kept whole)
+__device__ __forceinline__ uint32_t min32r(uint32_t x, const DevMod &M) {
+    const uint32_t r = mad32(__umulhi(x, M.mu32), 0u - M.m, x);
+    return min(r, r - M.m);
+}
+
 template <class IT, bool SPLIT, bool LAZY>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
 k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict__ partial) {
@@ -229,7 +243,7 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict_
     const uint4 *pq = reinterpret_cast<const uint4 *>(op.pent);
     constexpr uint32_t HC = panel_hc<SPLIT>();
     for (uint32_t i = gt; i < AW * (g.R + 1); i += PANEL_GT) acc[i] = 0;
-    auto bar_group = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(PANEL_GT)); };
+    auto bar_group = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(PANEL_GT) : "memory"); };
     // Software pipeline over a group's tiles: the first QR quads per thread
     // of its next tile (the whole tile when it has <= QR * PANEL_GT quads)
     // are loaded into registers before the current tile's write-out, so the
@@ -322,10 +336,10 @@ k_panel(DevPanel op, DevMod M, const uint32_t *__restrict__ xin, IT *__restrict_
                                      reinterpret_cast<uint4 *>(out) + v),
                                  "r"(res[0]), "r"(res[1]), "r"(res[2]), "r"(res[3]), "l"(POLICY_EVICT_LAST));
                 } else {
-                    res[0] = mod32_min(s4.x, M);
-                    res[1] = mod32_min(s4.y, M);
-                    res[2] = mod32_min(s4.z, M);
-                    res[3] = mod32_min(s4.w, M);
+                    res[0] = min32r(s4.x, M);
+                    res[1] = min32r(s4.y, M);
+                    res[2] = min32r(s4.z, M);
+                    res[3] = min32r(s4.w, M);
                     if constexpr (sizeof(IT) == 1) {
                         asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(
                                          reinterpret_cast<uint32_t *>(out) + v),
@@ -359,25 +373,21 @@ __global__ void k_panel_reduce(const IT *__restrict__ partial, uint32_t P, uint3
         uint64_t s[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) s[i] = 0;
-        // P residues < 2^32: exact in u64; four panels' loads in flight
-        uint32_t p = 0;
-        for (; p + 4 <= P; p += 4) {
-            uint4 e4[4];
+        // P residues < 2^32: exact in u64; eight panels' loads in flight
+        // (the partials are L2-resident: latency, not bandwidth, bounds this)
+        constexpr uint32_t CH = 8;
+        for (uint32_t p = 0; p < P; p += CH) {
+            uint4 e4[CH];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                e4[j] = __ldcs(reinterpret_cast<const uint4 *>(partial + (uint64_t)(p + j) * rows_pad) + v);
+            for (uint32_t j = 0; j < CH; ++j)
+                e4[j] = p + j < P ? __ldcs(reinterpret_cast<const uint4 *>(partial + (uint64_t)(p + j) * rows_pad) + v)
+                                  : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (uint32_t j = 0; j < CH; ++j) {
                 const IT *e = reinterpret_cast<const IT *>(&e4[j]);
 #pragma unroll
                 for (int i = 0; i < VEC; ++i) s[i] += e[i];
             }
-        }
-        for (; p < P; ++p) {
-            const uint4 e4 = __ldcs(reinterpret_cast<const uint4 *>(partial + (uint64_t)p * rows_pad) + v);
-            const IT *e = reinterpret_cast<const IT *>(&e4);
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) s[i] += e[i];
         }
         const uint32_t r0 = v * VEC;
         if (y_aligned && r0 + VEC <= rows) {

@@ -18,11 +18,23 @@ PanelGeom panel_geometry(uint64_t rows, uint64_t cols, uint32_t m, const BuildOp
     // accumulators + dummy row of the kernel's two thread groups) + the
     // tile-header cache (PANEL_HC) <= 227 KB.  Packed word: byte offset (< W * xbytes) above rs
     // row bits, R < 2^rs.
-    if (g.xbytes == 1) { g.W = 196608u; g.rs = 14; g.R = 4088u; }
-    else if (g.xbytes == 2) { g.W = 65536u; g.rs = 15; g.R = 8160u; }
-    else { g.W = 49152u; g.rs = 14; g.R = 2200u; }
-    if (bo.panel_cols) g.W = std::min<uint32_t>(bo.panel_cols, g.W);
-    if (bo.panel_rows) g.R = std::min<uint32_t>(bo.panel_rows, g.R);
+    if (g.xbytes == 1) { g.W = 196608u; g.R = 4088u; }
+    else if (g.xbytes == 2) { g.W = 65536u; g.R = 8160u; }
+    else { g.W = 49152u; g.R = 2200u; }
+    // explicit geometry (tuning / tests): R first, then W shrunk to the
+    // shared-memory budget and to the bits the row field leaves
+    if (bo.panel_rows) g.R = bo.panel_rows;
+    if (bo.panel_cols) {
+        const uint64_t acc = 2ull * (((1 + g.split) * (g.R + 1ull) + 3) / 4 * 4) * 4;
+        const uint64_t hc = (g.split ? 16u : 64u) * 32u + 16u;
+        const uint64_t fit = acc + hc < PANEL_SMEM_MAX ? (PANEL_SMEM_MAX - acc - hc) / g.xbytes / 32 * 32 : 32;
+        g.W = (uint32_t)std::min<uint64_t>(bo.panel_cols, fit);
+    }
+    // row field: the smallest rs with R (the dummy row) < 2^rs; the byte
+    // offset of x takes the remaining 32 - rs bits
+    g.rs = 1;
+    while ((1u << g.rs) <= g.R) ++g.rs;
+    while ((uint64_t)g.W * g.xbytes > (1ull << (32 - g.rs))) g.W -= 32;
     g.P = (uint32_t)((cols + g.W - 1) / g.W);
     g.B = (uint32_t)((rows + g.R - 1) / g.R);
     g.nctas = std::max<uint32_t>(1, nsm);
