@@ -175,3 +175,99 @@ def sequence_rows(n, row_idx, col_idx, vals, m, X, L, U, backend, group=None, wa
     if want_vout:
         return S, backend.to_numpy(V)
     return S
+
+
+def grid_shape(world: int, k: int, n: int = 0, nnz: int = 0, iterate_bytes: int = 2,
+               matrix_bytes_per_nnz: float = 5.4, hbm_gbs: float = 6500.0, nvlink_gbs: float = 900.0):
+    """P_r x P_c factorisation of the world for the 2-D mode, chosen by the
+    per-step byte model of SURVEY §8e: per GPU the HBM moves matrix / P_r plus
+    its column block of the iterate (read in full, band written), and the
+    NVLink ingress is (P_r - 1) / P_r of N x k / P_c iterate entries; the step
+    time is the larger of the two.  Ties prefer fewer column blocks (a bigger
+    block per GPU keeps the SpMM's nonzero reuse).  Without sizes (n = 0) the
+    model degenerates to 'most column blocks', P_c <= k."""
+    best, best_t = (world, 1), None
+    for pc in range(1, world + 1):
+        if world % pc or pc > max(1, k):
+            continue
+        pr = world // pc
+        vb = n * (k / pc) * iterate_bytes
+        hbm = nnz * matrix_bytes_per_nnz / pr + vb * (1 + 1 / pr)
+        nvl = vb * (pr - 1) / pr
+        t = max(hbm / hbm_gbs, nvl / nvlink_gbs) if n else -pc
+        if best_t is None or t < best_t - 1e-12:
+            best, best_t = (pr, pc), t
+    return best
+
+
+def sequence_2d(n, row_idx, col_idx, vals, m, X, L, U, backend, pr, pc, group=None, want_vout=False):
+    """2-D sequence on a P_r x P_c grid of ranks (rank = i * P_c + j): rank
+    (i, j) owns row band i of A (nnz-balanced) and column block j of X.  Per
+    step it computes its band of V_{t+1}[:, block j] and all-gathers the bands
+    among the P_r ranks of column block j (the exchange moves (P_r-1)/P_r of
+    N x k/P_c instead of N x k); the band projections U[band i]^T V[band i,
+    block j] are summed mod m over i once at the end.  P_r = 1 is the column
+    mode, P_c = 1 the row mode.  Returns S (L x ku x
+    k) on every rank (and V_L if asked)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if pr * pc != world:
+        raise ValueError(f"grid {pr} x {pc} does not match world size {world}")
+    X = np.asarray(X, dtype=np.uint32)
+    k = X.shape[1]
+    U = X if U is None else np.asarray(U, dtype=np.uint32)
+    ku = U.shape[1]
+    i, j = divmod(rank, pc)
+    b = row_bands(row_idx, n, pr)
+    c = column_shards(k, pc)
+    counts = [int(b[r + 1] - b[r]) for r in range(pr)]
+    lo, hi = int(b[i]), int(b[i + 1])
+    c0, c1 = int(c[j]), int(c[j + 1])
+    w = c1 - c0
+    # one all-gather group per column block (every rank creates every group,
+    # in the same order, as torch.distributed requires)
+    base = dist.get_process_group_ranks(group) if group is not None else list(range(world))
+    col_groups = [dist.new_group([base[r * pc + jj] for r in range(pr)]) for jj in range(pc)]
+    ri, ci, v = band_triples(row_idx, col_idx, vals, lo, hi)
+    A_band = backend.create(hi - lo, n, ri, ci, v, m)
+    dev = getattr(backend, "device", torch.device("cpu"))
+    wmax = max(1, int(max(c[1:] - c[:-1])))
+    S_part = torch.zeros((L, ku, wmax), dtype=torch.int32, device=dev)
+    V = None
+    if w:
+        V = backend.tensor(X[:, c0:c1])                 # column block j, replicated over i
+        U_band = backend.tensor(U[lo:hi])
+        S_band = backend.empty((L, ku, w))
+        for t in range(L):
+            backend.project(A_band, V[lo:hi], U_band, S_band[t])
+            if t + 1 < L or want_vout:
+                out = backend.empty((hi - lo, w))
+                backend.apply_block(A_band, V, out)
+                V = _all_gather_rows(col_groups[j], out, counts)
+        S_part[:, :, :w] = S_band
+    parts = [torch.empty_like(S_part) for _ in range(world)]
+    dist.all_gather(parts, S_part, group=group)
+    S = np.zeros((L, ku, k), np.uint32)
+    for jj in range(pc):
+        wj = int(c[jj + 1] - c[jj])
+        if not wj or not L:
+            continue
+        stack = torch.stack([parts[r * pc + jj][:, :, :wj].contiguous() for r in range(pr)])
+        out = backend.empty((L, ku, wj))
+        backend.sum_mod(A_band, stack, out)             # sum over row bands, mod m, on device
+        S[:, :, c[jj]:c[jj + 1]] = backend.to_numpy(out)
+    if want_vout:
+        # V_L: gather the column blocks (row group 0 holds each block complete)
+        vb = torch.zeros((n, wmax), dtype=torch.int32, device=dev)
+        if w:
+            vb[:, :w] = V
+        vparts = [torch.empty_like(vb) for _ in range(world)]
+        dist.all_gather(vparts, vb, group=group)
+        Vout = np.zeros((n, k), np.uint32)
+        for jj in range(pc):
+            wj = int(c[jj + 1] - c[jj])
+            Vout[:, c[jj]:c[jj + 1]] = vparts[jj].cpu().numpy().view(np.uint32)[:, :wj]
+        return S, Vout
+    return S

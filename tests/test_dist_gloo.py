@@ -79,6 +79,10 @@ def _worker(rank, world, port, mode, case, result_q):
         if mode == "rows":
             S, V = fd.sequence_rows(n, ri, ci, v, m, X, L, U, be, want_vout=True)
             result_q.put((rank, S, V))
+        elif mode.startswith("2d"):
+            pr, pc = (int(t) for t in mode[2:].split("x"))
+            S, V = fd.sequence_2d(n, ri, ci, v, m, X, L, U, be, pr, pc, want_vout=True)
+            result_q.put((rank, S, V))
         else:
             S = fd.sequence_columns(n, ri, ci, v, m, X, L, U, be)
             result_q.put((rank, S, None))
@@ -149,3 +153,28 @@ def test_rows_mode_uneven_world2(oracle_mod):
     want = oracle_mod.sequence(n, ri, ci, v, m, X, 5)
     for rank, S, V in _run("rows", case):
         assert np.array_equal(np.asarray(S).reshape(want.shape), want)
+
+
+@pytest.mark.parametrize("grid", ["2d2x2", "2d1x2", "2d2x1", "2d4x1"])
+def test_sequence_2d_matches_oracle(oracle_mod, grid):
+    # P_r x P_c grid (world 4 or 2): row bands x column blocks, all-gather of
+    # the iterate within each column block, projections summed over bands
+    pr, pc = (int(t) for t in grid[2:].split("x"))
+    case = _case(n=53, k=5, ku=3, L=5, m=2147483647, seed=11)
+    n, ri, ci, v, m, X, U, L = case
+    want, Vw = oracle_mod.sequence(n, ri, ci, v, m, X, L, U, want_vout=True)
+    for rank, S, V in _run(grid, case, world=pr * pc):
+        assert np.array_equal(np.asarray(S).reshape(want.shape), want), f"rank {rank}"
+        assert np.array_equal(V, Vw), f"rank {rank}"
+
+
+def test_grid_shape():
+    from paper_1004_3719_b200 import dist as fd
+    # c5 sizes (N = 2^21, ~21 M nnz, k = 16, u16 iterate): the byte model of
+    # SURVEY §8e picks 2 x 4 at P = 8 (NVLink-bound 8 x 1, matrix-bound 1 x 8)
+    assert fd.grid_shape(8, 16, n=1 << 21, nnz=21_000_000) == (2, 4)
+    for w in (1, 2, 4, 8):
+        pr, pc = fd.grid_shape(w, 16, n=1 << 21, nnz=21_000_000)
+        assert pr * pc == w and pc <= 16
+    assert fd.grid_shape(8, 1, n=1 << 21, nnz=21_000_000) == (8, 1)    # one column: rows only
+    assert fd.grid_shape(4, 16) == (1, 4)                              # no sizes: columns first
