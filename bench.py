@@ -198,18 +198,23 @@ def bench_ours(args):
         torch.distributed.barrier()
     units_per_step = 2 * info["nnz"]             # apply + transpose
     value = units_per_step * world * args.steps / (total_ms / 1e3)
-    alg = info["alg_bytes_apply"] + info["alg_bytes_transpose"]
-    kern_ms = float(t.sum(axis=1).mean())        # the two apply calls of a step
-    achieved = alg / (kern_ms / 1e3) / 1e9
+    # roofline of the dominant kernel pair (k_panel + k_panel_reduce of the
+    # y <- A x call): algorithmic bytes of one launch / its mean event time;
+    # traffic = ncu DRAM bytes of the same launch (profiles/ncu_traffic.json)
+    alg = info["alg_bytes_apply"]
+    apply_ms = float(t[:, 0].mean())
+    achieved = alg / (apply_ms / 1e3) / 1e9
     panels = info["strategy_apply"] == ff.STRATEGY_PANELS
-    kname = ("k_panel + k_panel_reduce (x panels in shared memory; A and A^T calls)" if panels
-             else "k_apply (rows layout; A and A^T calls)")
+    kname = ("k_panel + k_panel_reduce (x panels in shared memory), y <- A x" if panels
+             else "k_apply (rows layout), y <- A x")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": ncu_traffic(f"{cfg}_apply"),
                 "kernel": kname, "peak_source": peak_src,
-                "alg_bytes_per_step": alg,
-                "apply_ms": round(float(t[:, 0].mean()), 5),
-                "transpose_ms": round(float(t[:, 1].mean()), 5)}
+                "alg_bytes_per_launch": alg,
+                "alg_bytes_note": "4 B per +-1 nonzero, 4 + e_v B per valued nonzero, 4 B per x and y element",
+                "apply_ms": round(apply_ms, 5),
+                "transpose_ms": round(float(t[:, 1].mean()), 5),
+                "transpose_alg_gbs": round(info["alg_bytes_transpose"] / (float(t[:, 1].mean()) / 1e3) / 1e9, 1)}
 
     out = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
