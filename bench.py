@@ -237,10 +237,55 @@ def bench_ours(args):
         out["cpu_baseline"] = cpu_baseline(M, budget_s=args.cpu_seconds)
         if not args.no_extras:
             out["extras"] = extras(ff, flush, stream, hbm_peak, args)
+    if world > 1 and not args.no_extras:
+        out["extras"] = {"c5_sequence_2d": _seq_dist(args, world, rank, local)}
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _seq_dist(args, world, rank, local):
+    """c5 block Wiedemann sequence across the ranks (dist.sequence_2d on the
+    P_r x P_c grid grid_shape picks): steps/s over the timed steps of one
+    sequence call (device events on each rank, max over ranks), after
+    args.warmup warm-up steps.  Reported beside the headline, never instead of
+    it; a failure is reported, not raised."""
+    import torch
+
+    import synth
+    from paper_1004_3719_b200 import dist as fdist
+    try:
+        M = synth.config_matrix("c5")
+        n, m, k = M["rows"], M["m"], 16
+        g = synth.rng(2005)
+        X = synth.uniform(g, (n, k), m)
+        U = synth.uniform(g, (n, k), m)
+        steps = max(1, min(args.steps, 50))
+        L = args.warmup + steps
+        pr, pc = fdist.grid_shape(world, k, n=n, nnz=len(M["row"]), iterate_bytes=4)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def hook(t):
+            if t == args.warmup:
+                torch.cuda.synchronize()
+                torch.distributed.barrier()
+                e0.record()
+            elif t == L:
+                e1.record()
+                torch.cuda.synchronize()
+
+        fdist.sequence_2d(n, M["row"], M["col"], M["val"], m, X, L, U,
+                          fdist.CudaBackend(f"cuda:{local}"), pr, pc, on_step=hook)
+        ms = e0.elapsed_time(e1)
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+        return {"steps_per_s": steps / (ms / 1e3), "ms_per_step": ms / steps, "steps": steps,
+                "grid": [pr, pc], "k": k, "mode": "2-D (row bands x column blocks), NCCL all-gather per step",
+                "scaling": "strong (one c5 problem split over the ranks)"}
+    except Exception as e:                       # the headline line must still print
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def _rank_matrix(cfg, rank):

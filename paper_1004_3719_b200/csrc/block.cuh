@@ -414,4 +414,15 @@ int launch_block_t(const DevOp &op, const DevMod &M, uint32_t k, uint32_t alpha,
     return (int)cudaGetLastError();
 }
 
+// Explicit instantiations live in block.cu (u32 -> u32) and block16.cu (u16
+// iterates), so seq.cu does not recompile the ~90 block kernels (build time).
+#define FFSPMV_BLOCK_LAUNCH(TX, TY)                                                              \
+    int launch_block_t<TX, TY>(const DevOp &, const DevMod &, uint32_t, uint32_t, const TX *,  \
+                               uint64_t, uint32_t, TY *, uint64_t, void *)
+#ifndef FFSPMV_BLOCK_INSTANTIATE
+extern template FFSPMV_BLOCK_LAUNCH(uint32_t, uint32_t);
+extern template FFSPMV_BLOCK_LAUNCH(uint16_t, uint16_t);
+extern template FFSPMV_BLOCK_LAUNCH(uint16_t, uint32_t);
+#endif
+
 }  // namespace ffspmv

@@ -200,7 +200,8 @@ def grid_shape(world: int, k: int, n: int = 0, nnz: int = 0, iterate_bytes: int 
     return best
 
 
-def sequence_2d(n, row_idx, col_idx, vals, m, X, L, U, backend, pr, pc, group=None, want_vout=False):
+def sequence_2d(n, row_idx, col_idx, vals, m, X, L, U, backend, pr, pc, group=None, want_vout=False,
+                on_step=None):
     """2-D sequence on a P_r x P_c grid of ranks (rank = i * P_c + j): rank
     (i, j) owns row band i of A (nnz-balanced) and column block j of X.  Per
     step it computes its band of V_{t+1}[:, block j] and all-gathers the bands
@@ -208,7 +209,9 @@ def sequence_2d(n, row_idx, col_idx, vals, m, X, L, U, backend, pr, pc, group=No
     N x k/P_c instead of N x k); the band projections U[band i]^T V[band i,
     block j] are summed mod m over i once at the end.  P_r = 1 is the column
     mode, P_c = 1 the row mode.  Returns S (L x ku x
-    k) on every rank (and V_L if asked)."""
+    k) on every rank (and V_L if asked).  ``on_step(t)``, if given, is
+    called before step t and once more with t = L after the last one (the
+    bench brackets its timed steps with device events there)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -241,11 +244,15 @@ def sequence_2d(n, row_idx, col_idx, vals, m, X, L, U, backend, pr, pc, group=No
         U_band = backend.tensor(U[lo:hi])
         S_band = backend.empty((L, ku, w))
         for t in range(L):
+            if on_step is not None:
+                on_step(t)
             backend.project(A_band, V[lo:hi], U_band, S_band[t])
             if t + 1 < L or want_vout:
                 out = backend.empty((hi - lo, w))
                 backend.apply_block(A_band, V, out)
                 V = _all_gather_rows(col_groups[j], out, counts)
+        if on_step is not None:
+            on_step(L)
         S_part[:, :, :w] = S_band
     parts = [torch.empty_like(S_part) for _ in range(world)]
     dist.all_gather(parts, S_part, group=group)

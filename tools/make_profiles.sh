@@ -21,8 +21,8 @@ timeout 300 $NCU --set full --import-source on -k regex:k_block -s 2 -c 1 --csv 
     python tools/prof.py --config c4 --op block --k 16 --reps 3 > $OUT/c4_block16_raw.csv 2>/dev/null
 timeout 300 $NCU --set full --import-source on -k regex:k_block -s 2 -c 1 --csv --page source --print-source sass \
     python tools/prof.py --config c4 --op block --k 16 --reps 3 > $OUT/c4_block16_sass.csv 2>/dev/null
-timeout 300 $NCU --set full --import-source on -k regex:k_seq_step_mma -s 2 -c 1 --csv --page raw \
+timeout 300 $NCU --set full --import-source on -k regex:k_seq_step -s 2 -c 1 --csv --page raw \
     python tools/prof.py --config c5 --op sequence --k 16 --reps 1 --steps 4 > $OUT/c5_seq_raw.csv 2>/dev/null
-timeout 300 $NCU --set full --import-source on -k regex:k_seq_step_mma -s 2 -c 1 --csv --page source --print-source sass \
+timeout 300 $NCU --set full --import-source on -k regex:k_seq_step -s 2 -c 1 --csv --page source --print-source sass \
     python tools/prof.py --config c5 --op sequence --k 16 --reps 1 --steps 4 > $OUT/c5_seq_sass.csv 2>/dev/null
 ls -la $OUT

@@ -20,7 +20,10 @@ ap.add_argument("--op", default="apply", choices=["apply", "transpose", "block",
 ap.add_argument("--k", type=int, default=16)
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--steps", type=int, default=4)
+ap.add_argument("--lib", default=None)
 a = ap.parse_args()
+if a.lib:
+    ff.load(a.lib)
 
 M = synth.config_matrix(a.config)
 m, rows, cols = M["m"], M["rows"], M["cols"]
