@@ -1,7 +1,6 @@
-# scratch gpurun job: tests after the block TU split + L2 working-set probe for the sequence step
+# scratch gpurun job: round-end check of the committed tree (tests, bench, smoke, block A/B)
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; echo "tests rc=$?" >> gpurun_out/gputest.log
-timeout 300 python tools/time_seq.py --config c5 --k 16 --steps 200 >> gpurun_out/seq_l2.jsonl 2>>gpurun_out/seq_l2.err
-timeout 300 python tools/time_seq.py --config c5 --k 8 --steps 200 >> gpurun_out/seq_l2.jsonl 2>>gpurun_out/seq_l2.err
-timeout 300 python tools/time_seq.py --config c2 --k 16 --steps 200 >> gpurun_out/seq_l2.jsonl 2>>gpurun_out/seq_l2.err
-timeout 300 python tools/time_seq.py --config c2 --k 8 --steps 200 >> gpurun_out/seq_l2.jsonl 2>>gpurun_out/seq_l2.err
+timeout 600 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+timeout 300 python tools/time_block.py > gpurun_out/blk_final.jsonl 2>&1
