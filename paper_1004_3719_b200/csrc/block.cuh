@@ -355,10 +355,10 @@ __device__ __forceinline__ void block_slice_vec(const DevOp &op, const DevMod &M
 // Vector kernel: slices take the CPL path with KPV lanes per row; the rare
 // long rows / CSR groups / zero rows keep the scalar path (KP lanes per row).
 // Occupancy bound per width (measured, tools/time_block.py at c4, m = 2^31-1):
-// 8 CTAs/SM (64 registers) for k <= 8, 6 CTAs/SM (80 registers) above; the
+// 8 CTAs/SM (64 registers) for k <= 8, 5 CTAs/SM (96 registers) above; the
 // few spills cost less than the latency the extra warps hide on the X gathers.
 template <class VT, int KPV, int CPL, int KP, class TX, class TY>
-__global__ void __launch_bounds__(BWARPS * 32, (KP <= 8 ? 8 : 6))
+__global__ void __launch_bounds__(BWARPS * 32, (KP <= 8 ? 8 : 5))
 k_block_vec(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint32_t ldx,
             BlockOut<TY> out) {
     uint32_t w = blockIdx.x * BWARPS + (threadIdx.x >> 5);

@@ -1,6 +1,6 @@
-# scratch gpurun job: round-end check of the committed tree (tests, bench, smoke, block A/B)
+# scratch gpurun job: round-end check of the committed tree (tests, bench, smoke)
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; echo "tests rc=$?" >> gpurun_out/gputest.log
 timeout 600 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
-timeout 300 python tools/time_block.py > gpurun_out/blk_final.jsonl 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 3 --warmup 3 --cpu-seconds 0.5 > /dev/null 2>&1
