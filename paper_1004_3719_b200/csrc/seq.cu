@@ -97,6 +97,83 @@ k_project(const IT *__restrict__ V, const IT *__restrict__ Uc, uint64_t n, uint3
     }
 }
 
+// Register-tiled projection for k, ku <= 64 (the common case): thread
+// (g, ta, tb) owns the 4 x 4 block of pairs a in [4ta, 4ta+4), b in [4tb, 4tb+4)
+// for the rows r = g (mod G) of each staged tile, so a row costs two 16-byte
+// shared loads per 16 exact MACs (instead of two 4-byte loads per MAC); the G
+// row groups' residues are summed (< G m < 2^64) at the end.  Same partial
+// layout and exactness argument as k_project.
+constexpr uint32_t PROJ_TR = 64;
+
+template <class IT, class Acc>
+__global__ void __launch_bounds__(PROJ_THREADS)
+k_project_t(const IT *__restrict__ V, const IT *__restrict__ Uc, uint64_t n, uint32_t k,
+            uint32_t ku, uint32_t ldu, uint32_t tr, bool vec, DevMod M, uint32_t *__restrict__ partial) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const uint32_t K4 = (k + 3) & ~3u, KU4 = (ku + 3) & ~3u;
+    uint32_t *su = sm;                         // tr x KU4 (zero padded)
+    uint32_t *sv = sm + tr * KU4;              // tr x K4
+    const uint32_t ntb = K4 / 4, nt = (KU4 / 4) * ntb;
+    const uint32_t G = PROJ_THREADS / nt;      // row groups, >= 1 (k, ku <= 64)
+    const uint32_t tid = threadIdx.x, g = tid / nt, tt = tid - g * nt;
+    const uint32_t ta = tt / ntb, tb = tt - ta * ntb;
+    const bool active = g < G;
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t r0 = min(n, (uint64_t)blockIdx.x * per), r1 = min(n, r0 + per);
+    Acc acc[16];
+    for (uint64_t rb = r0; rb < r1; rb += tr) {
+        const uint32_t nr = (uint32_t)min((uint64_t)tr, r1 - rb);
+        __syncthreads();
+        if (vec) {
+            // u32, k and ku multiples of 4, U unpadded: both tiles are
+            // contiguous runs of 16-byte vectors (zero beyond nr rows)
+            const uint4 *u4 = reinterpret_cast<const uint4 *>(Uc + rb * ldu);
+            const uint4 *v4 = reinterpret_cast<const uint4 *>(V + rb * k);
+            const uint32_t nu = nr * KU4 / 4, nv = nr * K4 / 4;
+            for (uint32_t i = tid; i < tr * KU4 / 4; i += PROJ_THREADS)
+                reinterpret_cast<uint4 *>(su)[i] = i < nu ? __ldcs(u4 + i) : make_uint4(0, 0, 0, 0);
+            for (uint32_t i = tid; i < tr * K4 / 4; i += PROJ_THREADS)
+                reinterpret_cast<uint4 *>(sv)[i] = i < nv ? __ldcs(v4 + i) : make_uint4(0, 0, 0, 0);
+        } else {
+            for (uint32_t i = tid; i < tr * KU4; i += PROJ_THREADS) {
+                const uint32_t r = i / KU4, c = i - r * KU4;
+                su[i] = (r < nr && c < ku) ? (uint32_t)Uc[(rb + r) * ldu + c] : 0u;
+            }
+            for (uint32_t i = tid; i < tr * K4; i += PROJ_THREADS) {
+                const uint32_t r = i / K4, c = i - r * K4;
+                sv[i] = (r < nr && c < k) ? (uint32_t)V[(rb + r) * k + c] : 0u;
+            }
+        }
+        __syncthreads();
+        if (active) {
+            for (uint32_t r = g; r < nr; r += G) {
+                const uint4 u = *reinterpret_cast<const uint4 *>(su + r * KU4 + 4 * ta);
+                const uint4 v = *reinterpret_cast<const uint4 *>(sv + r * K4 + 4 * tb);
+                const uint32_t ua[4] = {u.x, u.y, u.z, u.w}, vb[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i * 4 + j].mad(ua[i], vb[j]);
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t *red = sm;                        // (G * nt) x 16 residues
+    if (active) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) red[tid * 16 + q] = acc[q].reduce(M);
+    }
+    __syncthreads();
+    const uint32_t pairs = ku * k;
+    for (uint32_t p = tid; p < pairs; p += PROJ_THREADS) {
+        const uint32_t a = p / k, b = p - a * k;
+        const uint32_t t2 = (a >> 2) * ntb + (b >> 2), q = (a & 3) * 4 + (b & 3);
+        uint64_t sacc = 0;
+        for (uint32_t gg = 0; gg < G; ++gg) sacc += red[(gg * nt + t2) * 16 + q];
+        partial[(uint64_t)blockIdx.x * pairs + p] = mod64(sacc, M);
+    }
+}
+
 // S_t[p] = sum_c partial[c][p] mod m: one warp per output pair.
 __global__ void k_seq_finalize(const uint32_t *__restrict__ partial, uint32_t nctas,
                                uint32_t pairs, DevMod M, uint32_t *__restrict__ S) {
@@ -255,7 +332,18 @@ int project(const IT *V, const IT *Uc, uint32_t ldu, const DevMod &M, uint64_t n
     uint64_t per = (n + nctas - 1) / nctas;
     typedef unsigned __int128 u128;
     bool wide = (u128)per * (u128)(M.m - 1) * (u128)(M.m - 1) > (u128)~(uint64_t)0;
-    if (wide)
+    if (k <= 64 && ku <= 64) {
+        const uint32_t K4 = (k + 3) & ~3u, KU4 = (ku + 3) & ~3u;
+        // 8192-word row tiles (32 KB): a few 16-byte loads in flight per thread
+        const uint32_t trt = std::max<uint32_t>(PROJ_TR, std::min<uint32_t>(512, 8192 / (K4 + KU4)));
+        const bool vec = sizeof(IT) == 4 && K4 == k && KU4 == ku && ldu == ku &&
+                         ((uintptr_t)V & 15) == 0 && ((uintptr_t)Uc & 15) == 0;
+        const size_t sm_t = std::max<size_t>((size_t)trt * (K4 + KU4), (size_t)PROJ_THREADS * 16) * 4;
+        if (wide)
+            k_project_t<IT, Acc96><<<nctas, PROJ_THREADS, sm_t, st>>>(V, Uc, n, k, ku, ldu, trt, vec, M, partial);
+        else
+            k_project_t<IT, Acc64><<<nctas, PROJ_THREADS, sm_t, st>>>(V, Uc, n, k, ku, ldu, trt, vec, M, partial);
+    } else if (wide)
         k_project<IT, Acc96><<<nctas, PROJ_THREADS, smem, st>>>(V, Uc, n, k, ku, ldu, tr, M, partial);
     else
         k_project<IT, Acc64><<<nctas, PROJ_THREADS, smem, st>>>(V, Uc, n, k, ku, ldu, tr, M, partial);
