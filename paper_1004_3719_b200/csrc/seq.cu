@@ -31,7 +31,7 @@ int num_sms() {
 }
 
 uint32_t proj_ctas(uint64_t n) {
-    uint64_t c = std::min<uint64_t>((uint64_t)num_sms() * 2, (n + 63) / 64);
+    uint64_t c = std::min<uint64_t>((uint64_t)num_sms() * 4, (n + 63) / 64);   // 4 CTAs/SM of k_project_t
     return (uint32_t)std::max<uint64_t>(1, c);
 }
 

@@ -1,4 +1,4 @@
-# scratch gpurun job: round-end check of the committed tree (tests, bench, smoke)
+# scratch gpurun job: round-end check of the committed tree (tests, bench, smoke, launch list)
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; echo "tests rc=$?" >> gpurun_out/gputest.log
 timeout 600 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
