@@ -2,28 +2,35 @@
 """Benchmark of the exact mod-m hot path (BASELINE.json metric).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
-                    [--config c2|c3] [--no-extras]
+                    [--no-extras] [--cpu-seconds S]
 
-Headline (N=1): BASELINE configs[1] -- synthetic 2^20 x 2^20 matrix,
-Poisson(10) row lengths, 30% +-1, mod 65521.  One step = y <- A x followed by
-y' <- A^T x' (the whole apply hot path), inputs resident
-in HBM.  L2 (126 MB) is flushed between timed steps by writing a 256 MB
-buffer, outside the step's events.  value = nonzeros processed per second
-(2 nnz per step per rank), times from CUDA events on the launching stream,
-max over ranks.  N > 1 (torchrun): every rank runs its own independent
-c2-shaped problem (rank-seeded) -- weak scaling, no data-path collective.
+N = 1 headline: BASELINE configs[2], the largest single-GPU configuration
+and the one the north star's 60 % HBM target is stated on -- the synthetic
+GL7d-shaped 1,911,130 x 1,955,309 matrix (skewed "c + r" rows, every nonzero
++-1 mod 3).  One step = y <- A x (the hybrid-format apply),
+inputs resident in HBM; L2 (126 MB) is flushed between timed steps by a
+256 MB write outside the step's events.  value = canonical nonzeros per
+second.  The dominant kernel's roofline, the e2e number through the
+host-buffer C-ABI call, the clocks and the oracle (threaded, all host
+cores) are on the same line; c2 apply + transpose, c4 block SpMM and the
+c5 block Wiedemann sequence (with its oracle seconds per step) are extras.
 
-Extras (default on, N = 1 only): c3 hybrid apply, c4 block apply k = 8/16/32,
-c5 sequence steps/s -- each with its own roofline fraction.
+N > 1 headline: BASELINE configs[4] -- the c5 block Wiedemann sequence
+(N = 2^21, k = 16, m = 65521) as ONE problem split over the N ranks
+(strong scaling), steps/s, device time max over ranks.  Its N = 1 point is
+extras.c5_sequence of the N = 1 line.  Without torchrun, ``--gpus N``
+relaunches itself under torch.distributed.run with N ranks.
 
---impl reference times the CPU oracle (oracle/, plain C, 1 thread) on the
-same config, rank 0 only.
+--impl reference times the CPU oracle (oracle/, plain C, u128, threaded
+timing mode on all host cores) on the same workload and metric, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -35,6 +42,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = "mod-m SpMV nonzeros/sec & achieved HBM GB/s vs peak; seq steps/s at 1/2/4/8"
 FLUSH_BYTES = 256 << 20
+HEADLINE = "c3"
+DESCRIBE = {
+    "c2": "c2: 2^20 x 2^20, Poisson(10) nnz/row, 30% +-1, mod 65521; y <- A x and y' <- A^T x'",
+    "c3": "c3: 1911130 x 1955309 GL7d-shaped, lognormal 'c + r' rows (mean ~19.5, 0.01% of "
+          "1000-4000), every nonzero +-1 mod 3; y <- A x (hybrid-format apply)",
+    "c4": "c4: 2^20 x 2^20, Poisson(10), 30% +-1, mod 2^31-1; Y <- A X, k = 8/16/32",
+    "c5": "c5: 2^21 x 2^21, Poisson(10), 30% +-1, mod 65521; block Wiedemann sequence "
+          "S_t = U^T A^t X, k = ku = 16",
+}
 
 
 def peaks():
@@ -48,7 +64,7 @@ def peaks():
 
 
 def ncu_traffic(key):
-    """dram bytes per launch of the dominant kernel from the committed ncu
+    """DRAM bytes per launch of the dominant kernel(s) from the committed ncu
     --set full summary (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -113,6 +129,16 @@ def dist_env():
     return world, rank, local
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------ ours ---
 
 def to_dev(a):
@@ -124,9 +150,10 @@ LAUNCHES = {"timed": 0}
 
 
 def timed_steps(step_fns, steps, warmup, flush, stream):
-    """Run warmup + steps of a list of launch closures.  Returns per-launch
-    event times (ms, shape steps x len(step_fns)); LAUNCHES["timed"] gets the
-    number of library kernels launched inside the timed steps."""
+    """Run warmup + steps of a list of launch closures, L2 flushed before each
+    step (outside the events).  Returns per-call event times (ms, steps x
+    len(step_fns)); LAUNCHES["timed"] = library kernels launched in the
+    timed steps."""
     import torch
 
     import paper_1004_3719_b200 as ff
@@ -146,15 +173,13 @@ def timed_steps(step_fns, steps, warmup, flush, stream):
             ev[s][j][1].record(stream)
     LAUNCHES["timed"] = ff.ffspmv_kernel_launches() - l0
     torch.cuda.synchronize()
-    t = np.array([[a.elapsed_time(b) for a, b in row] for row in ev])
-    return t
+    return np.array([[a.elapsed_time(b) for a, b in row] for row in ev])
 
 
 def bench_ours(args):
     import torch
 
     import paper_1004_3719_b200 as ff
-    import synth
 
     world, rank, local = dist_env()
     if world > 1:
@@ -164,215 +189,142 @@ def bench_ours(args):
     else:
         torch.cuda.set_device(0)
     ff.load()
-    stream = torch.cuda.current_stream()
-    hbm_peak, peak_src = peaks()
-    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-
-    cfg = args.config
-    M = synth.config_matrix(cfg) if world == 1 else _rank_matrix(cfg, rank)
-    m, rows, cols = M["m"], M["rows"], M["cols"]
-    A = ff.ffspmv_create(rows, cols, M["row"], M["col"], M["val"], m)
-    info = A.info()
-    g = synth.rng(synth.CONFIGS[cfg]["vseed"] + 7919 * rank)
-    x = to_dev(synth.uniform(g, cols, m))
-    xt = to_dev(synth.uniform(g, rows, m))
-    y = torch.empty(rows, dtype=torch.int32, device="cuda")
-    yt = torch.empty(cols, dtype=torch.int32, device="cuda")
-    fns = [lambda: ff.ffspmv_apply(A, 1, x, 0, y, stream),
-           lambda: ff.ffspmv_apply_transpose(A, 1, xt, 0, yt, stream)]
-
-    # timed region: barrier + sync on both sides, device events per launch
     if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t = timed_steps(fns, args.steps, args.warmup, flush, stream)
-    launches = LAUNCHES["timed"]
-    torch.cuda.synchronize()
-    step_ms = float(t.sum(axis=1).mean())
-    total_ms = float(t.sum())
-    if world > 1:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(tt.item())
-        torch.distributed.barrier()
-    units_per_step = 2 * info["nnz"]             # apply + transpose
-    value = units_per_step * world * args.steps / (total_ms / 1e3)
-    # roofline of the dominant kernel pair (k_panel + k_panel_reduce of the
-    # y <- A x call): algorithmic bytes of one launch / its mean event time;
-    # traffic = ncu DRAM bytes of the same launch (profiles/ncu_traffic.json)
-    alg = info["alg_bytes_apply"]
-    apply_ms = float(t[:, 0].mean())
-    achieved = alg / (apply_ms / 1e3) / 1e9
-    panels = info["strategy_apply"] == ff.STRATEGY_PANELS
-    kname = ("k_panel + k_panel_reduce (x panels in shared memory), y <- A x" if panels
-             else "k_apply (rows layout), y <- A x")
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": ncu_traffic(f"{cfg}_apply"),
-                "kernel": kname, "peak_source": peak_src,
-                "alg_bytes_per_launch": alg,
-                "alg_bytes_note": "4 B per +-1 nonzero, 4 + e_v B per valued nonzero, 4 B per x and y element",
-                "apply_ms": round(apply_ms, 5),
-                "transpose_ms": round(float(t[:, 1].mean()), 5),
-                "transpose_alg_gbs": round(info["alg_bytes_transpose"] / (float(t[:, 1].mean()) / 1e3) / 1e9, 1)}
-
-    out = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-           "accumulator": f"u{info['acc_bits_max']}", "data": "synthetic",
-           "config": {"workload": f"{cfg}: " + _describe(cfg), "rows": rows, "cols": cols,
-                      "nnz": info["nnz"], "modulus": m, "op": "y <- A x ; y' <- A^T x'",
-                      "l2": "flushed between timed steps (256 MB write)",
-                      "parallelism": f"independent {cfg} problem per rank" if world > 1 else "1 GPU"},
-           "roofline": roofline, "gpu_launches": launches,
-           "mflops_paper_unit": 2 * value / 1e6}
-    out["clocks"] = clk.summary()
-    out["e2e"] = _e2e(ff, A, M, args, rows, cols, m, g, world)
-    out["plan"] = {k: info[k] for k in ("strategy_apply", "strategy_transpose", "panels",
-                                        "panel_bands", "gather_locality", "bands", "bands_sell",
-                                        "bands_csr", "bands_coos", "slices", "long_rows", "nnz_pm1",
-                                        "nnz_valued", "padded_slots", "stream_bytes",
-                                        "panel_stream_bytes", "create_seconds")}
-    if rank == 0 and world == 1:
-        out["cpu_baseline"] = cpu_baseline(M, budget_s=args.cpu_seconds)
-        if not args.no_extras:
-            out["extras"] = extras(ff, flush, stream, hbm_peak, args)
-    if world > 1 and not args.no_extras:
-        out["extras"] = {"c5_sequence_2d": _seq_dist(args, world, rank, local)}
+        out = bench_multi(args, world, rank, local)
+    else:
+        out = bench_single(args)
     if rank == 0:
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def _seq_dist(args, world, rank, local):
-    """c5 block Wiedemann sequence across the ranks (dist.sequence_2d on the
-    P_r x P_c grid grid_shape picks): steps/s over the timed steps of one
-    sequence call (device events on each rank, max over ranks), after
-    args.warmup warm-up steps.  Reported beside the headline, never instead of
-    it; a failure is reported, not raised."""
+def bench_single(args):
+    """N = 1: c3 apply headline (see module docstring)."""
     import torch
 
+    import paper_1004_3719_b200 as ff
     import synth
-    from paper_1004_3719_b200 import dist as fdist
-    try:
-        M = synth.config_matrix("c5")
-        n, m, k = M["rows"], M["m"], 16
-        g = synth.rng(2005)
-        X = synth.uniform(g, (n, k), m)
-        U = synth.uniform(g, (n, k), m)
-        steps = max(1, min(args.steps, 50))
-        L = args.warmup + steps
-        pr, pc = fdist.grid_shape(world, k, n=n, nnz=len(M["row"]), iterate_bytes=4)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-        def hook(t):
-            if t == args.warmup:
-                torch.cuda.synchronize()
-                torch.distributed.barrier()
-                e0.record()
-            elif t == L:
-                e1.record()
-                torch.cuda.synchronize()
-
-        fdist.sequence_2d(n, M["row"], M["col"], M["val"], m, X, L, U,
-                          fdist.CudaBackend(f"cuda:{local}"), pr, pc, on_step=hook)
-        ms = e0.elapsed_time(e1)
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
-        return {"steps_per_s": steps / (ms / 1e3), "ms_per_step": ms / steps, "steps": steps,
-                "grid": [pr, pc], "k": k, "mode": "2-D (row bands x column blocks), NCCL all-gather per step",
-                "scaling": "strong (one c5 problem split over the ranks)"}
-    except Exception as e:                       # the headline line must still print
-        return {"error": f"{type(e).__name__}: {e}"[:300]}
-
-
-def _rank_matrix(cfg, rank):
-    import synth
-    c = dict(synth.CONFIGS[cfg])
-    saved = synth.CONFIGS[cfg]
-    try:
-        c["seed"] = saved["seed"] + 100 * rank
-        synth.CONFIGS[cfg] = c
-        return synth.config_matrix(cfg)
-    finally:
-        synth.CONFIGS[cfg] = saved
-
-
-def _describe(cfg):
-    return {
-        "c2": "2^20 x 2^20, Poisson(10) nnz/row, 30% +-1, mod 65521, apply + transpose apply",
-        "c3": "1911130 x 1955309 GL7d-shaped, lognormal rows (mean ~19.7), all +-1, mod 3",
-    }.get(cfg, cfg)
+    stream = torch.cuda.current_stream()
+    hbm_peak, peak_src = peaks()
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    M = synth.config_matrix(HEADLINE)
+    m, rows, cols = M["m"], M["rows"], M["cols"]
+    A = ff.ffspmv_create(rows, cols, M["row"], M["col"], M["val"], m, no_transpose=True)
+    info = A.info()
+    g = synth.rng(synth.CONFIGS[HEADLINE]["vseed"])
+    x = to_dev(synth.uniform(g, cols, m))
+    y = torch.empty(rows, dtype=torch.int32, device="cuda")
+    fns = [lambda: ff.ffspmv_apply(A, 1, x, 0, y, stream)]
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        t = timed_steps(fns, args.steps, args.warmup, flush, stream)
+    launches = LAUNCHES["timed"]
+    total_ms = float(t.sum())
+    nnz = info["nnz"]
+    value = nnz * args.steps / (total_ms / 1e3)
+    apply_ms = float(t[:, 0].mean())
+    alg = info["alg_bytes_apply"]
+    achieved = alg / (apply_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": ncu_traffic("c3_apply"),
+                "kernel": _apply_kernel_name(ff, info), "peak_source": peak_src,
+                "alg_bytes_per_launch": alg,
+                "alg_bytes_note": "4 B per +-1 nonzero, 4 + e_v B per valued nonzero, 4 B per x "
+                                  "and y element (DESIGN.md §6); one launch = one y <- A x",
+                "launch_ms": round(apply_ms, 5)}
+    out = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+           "accumulator": f"u{info['acc_bits_max']}", "data": "synthetic",
+           "config": {"workload": DESCRIBE[HEADLINE], "rows": rows, "cols": cols, "nnz": nnz,
+                      "modulus": m, "op": "y <- A x (alpha = 1, beta = 0)",
+                      "l2": "flushed between timed steps (256 MB write)", "parallelism": "1 GPU"},
+           "roofline": roofline, "gpu_launches": launches,
+           "mflops_paper_unit": 2 * value / 1e6, "clocks": clk.summary()}
+    out["e2e"] = _e2e(ff, A, args, rows, cols, m, g)
+    out["plan"] = {k: info[k] for k in ("strategy_apply", "panels", "panel_bands",
+                                        "gather_locality", "bands_sell", "bands_csr", "bands_coos",
+                                        "slices", "long_rows", "nnz_pm1", "nnz_valued",
+                                        "padded_slots", "stream_bytes", "panel_stream_bytes",
+                                        "create_seconds")}
+    out["cpu_baseline"] = cpu_baseline(M, budget_s=args.cpu_seconds)
+    del A, x, y, M
+    if not args.no_extras:
+        out["extras"] = extras(ff, flush, stream, hbm_peak, args)
+    return out
 
 
-def _e2e(ff, A, M, args, rows, cols, m, g, world):
-    """Same metric through the public host-buffer call: each step copies x
-    (and x') from pinned host memory, runs, and copies y (and y') back."""
+def _apply_kernel_name(ff, info):
+    if info["strategy_apply"] == ff.STRATEGY_RUNS:
+        return ("k_runs_pack + k_runs + k_runs_reduce (packed x panels in shared memory, "
+                "register row runs), y <- A x")
+    if info["strategy_apply"] == ff.STRATEGY_PANELS:
+        return "k_panel + k_panel_reduce (x panels in shared memory), y <- A x"
+    return "k_apply (rows layout), y <- A x"
+
+
+def _e2e(ff, A, args, rows, cols, m, g):
+    """The headline metric through the public host-buffer C-ABI call: each
+    step copies x from pinned host memory, runs y <- A x, copies y back
+    (ffspmv_apply_host, synchronous)."""
     import torch
+    import synth
     xs = torch.empty(cols, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    xts = torch.empty(rows, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     ys = torch.empty(rows, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    yts = torch.empty(cols, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    xs[:] = synth_uniform(g, cols, m)
-    xts[:] = synth_uniform(g, rows, m)
+    xs[:] = synth.uniform(g, cols, m)
     for _ in range(args.warmup):
         ff.ffspmv_apply_host(A, ff.OP_APPLY, 1, xs, 0, ys)
-        ff.ffspmv_apply_host(A, ff.OP_TRANSPOSE, 1, xts, 0, yts)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         ff.ffspmv_apply_host(A, ff.OP_APPLY, 1, xs, 0, ys)
-        ff.ffspmv_apply_host(A, ff.OP_TRANSPOSE, 1, xts, 0, yts)
     dt = time.perf_counter() - t0
-    if world > 1:
-        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        dt = float(tt.item())
     nnz = A.info()["nnz"]
-    return {"value": 2 * nnz * world * args.steps / dt, "unit": "nnz/s",
-            "h2d_bytes_per_step": 4 * (cols + rows), "d2h_bytes_per_step": 4 * (rows + cols),
-            "api": "ffspmv_apply_host (pinned host buffers, synchronous)"}
-
-
-def synth_uniform(g, n, m):
-    import synth
-    return synth.uniform(g, n, m)
+    return {"value": nnz * args.steps / dt, "unit": "nnz/s", "h2d_bytes_per_step": 4 * cols,
+            "d2h_bytes_per_step": 4 * rows,
+            "api": "ffspmv_apply_host (pinned host buffers, synchronous, copies in the timed region)"}
 
 
 def cpu_baseline(M, budget_s=10.0):
-    """The oracle as it stands (plain C, single thread) on the same matrix:
-    repeated apply + transpose until ~budget_s of CPU time."""
+    """The oracle as it stands (plain C, u128) on the same matrix and metric:
+    the threaded timing mode on all host cores (triples sorted by row
+    beforehand, outside the timing), repeated until ~budget_s; plus one
+    single-threaded apply for reference."""
     import oracle
     import synth
     m, rows, cols = M["m"], M["rows"], M["cols"]
     g = synth.rng(4242)
     x = synth.uniform(g, cols, m)
-    xt = synth.uniform(g, rows, m)
     oracle.build()
+    T = oracle.host_threads()
+    rs, cs, vs = oracle.sort_triples(M["row"], M["col"], M["val"])
+    t0 = time.perf_counter()
+    oracle.apply(rows, cols, M["row"], M["col"], M["val"], m, x)
+    single = time.perf_counter() - t0
     reps, t0 = 0, time.perf_counter()
     while True:
-        oracle.apply(rows, cols, M["row"], M["col"], M["val"], m, x)
-        oracle.apply_transpose(rows, cols, M["row"], M["col"], M["val"], m, xt)
+        oracle.apply_mt(rows, cols, rs, cs, vs, m, x, nthreads=T)
         reps += 1
         dt = time.perf_counter() - t0
         if dt >= budget_s:
             break
-    nnz_in = M["row"].size
-    return {"value": 2 * nnz_in * reps / dt, "unit": "nnz/s", "cores": 1, "kind": "oracle",
-            "sample": f"{reps} x (apply + transpose) of the full {M['name']} matrix "
-                      f"({nnz_in} triples), {dt:.1f} s", "cpu": _cpu_model()}
+    nnz = _canonical_nnz(M)
+    return {"value": nnz * reps / dt, "unit": "nnz/s", "cores": T, "kind": "oracle",
+            "sample": f"{reps} x y <- A x of the full {M['name']} matrix ({M['row'].size} triples), "
+                      f"threaded timing mode on {T} threads, {dt:.1f} s",
+            "single_thread_value": nnz / single, "cpu": _cpu_model()}
 
 
-def _cpu_model():
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return None
+def _canonical_nnz(M):
+    """Canonical nonzeros of a synthetic matrix (duplicates merged, residues
+    0 dropped): the unit both arms count (R19).  Host counting only."""
+    key = M["row"].astype(np.int64) * M["cols"] + M["col"]
+    order = np.argsort(key, kind="stable")
+    k, v = key[order], M["val"][order] % M["m"]
+    starts = np.flatnonzero(np.r_[True, k[1:] != k[:-1]])
+    sums = np.add.reduceat(v, starts) % M["m"]          # < 2^32 residues per key: int64-exact
+    return int(np.count_nonzero(sums))
 
 
 # ---------------------------------------------------------------- extras ---
@@ -380,28 +332,29 @@ def _cpu_model():
 def extras(ff, flush, stream, hbm_peak, args):
     import torch
 
+    import oracle
     import synth
     res = {}
-    # c3: GL7d-shaped hybrid apply (the "largest config" of the 60% target)
-    M = synth.config_matrix("c3")
-    A = ff.ffspmv_create(M["rows"], M["cols"], M["row"], M["col"], M["val"], M["m"], no_transpose=True)
+    # c2: apply + transpose apply (configs[1])
+    M = synth.config_matrix("c2")
+    A = ff.ffspmv_create(M["rows"], M["cols"], M["row"], M["col"], M["val"], M["m"])
     info = A.info()
-    g = synth.rng(2003)
+    g = synth.rng(2002)
     x = to_dev(synth.uniform(g, M["cols"], M["m"]))
+    xt = to_dev(synth.uniform(g, M["rows"], M["m"]))
     y = torch.empty(M["rows"], dtype=torch.int32, device="cuda")
-    t = timed_steps([lambda: ff.ffspmv_apply(A, 1, x, 0, y, stream)], min(args.steps, 50),
-                    args.warmup, flush, stream)
-    ms = float(t.mean())
-    res["c3_apply"] = {"nnz_per_s": info["nnz"] / (ms / 1e3), "ms": ms,
-                       "alg_gbs": info["alg_bytes_apply"] / (ms / 1e3) / 1e9,
-                       "frac": info["alg_bytes_apply"] / (ms / 1e3) / 1e9 / hbm_peak,
-                       "stream_gbs": (info["stream_bytes"] + 4 * (M["rows"] + M["cols"])) / (ms / 1e3) / 1e9,
-                       "traffic": ncu_traffic("c3_apply"),
-                       "plan": {k: info[k] for k in ("strategy_apply", "panels", "panel_bands",
-                                                     "bands_sell", "bands_csr", "bands_coos",
-                                                     "long_rows", "slices", "padded_slots")}}
-    del A, x, y, M
-    # c4: block SpMM, m = 2^31 - 1
+    yt = torch.empty(M["cols"], dtype=torch.int32, device="cuda")
+    t = timed_steps([lambda: ff.ffspmv_apply(A, 1, x, 0, y, stream),
+                     lambda: ff.ffspmv_apply_transpose(A, 1, xt, 0, yt, stream)],
+                    min(args.steps, 50), args.warmup, flush, stream)
+    ms_a, ms_t = float(t[:, 0].mean()), float(t[:, 1].mean())
+    res["c2_apply_transpose"] = {
+        "nnz_per_s": 2 * info["nnz"] / ((ms_a + ms_t) / 1e3), "apply_ms": ms_a,
+        "transpose_ms": ms_t, "frac_apply": info["alg_bytes_apply"] / (ms_a / 1e3) / 1e9 / hbm_peak,
+        "frac_transpose": info["alg_bytes_transpose"] / (ms_t / 1e3) / 1e9 / hbm_peak,
+        "traffic_apply": ncu_traffic("c2_apply"), "strategy": info["strategy_apply"]}
+    del A, x, xt, y, yt, M
+    # c4: block SpMM, m = 2^31 - 1 (configs[3])
     M = synth.config_matrix("c4")
     A = ff.ffspmv_create(M["rows"], M["cols"], M["row"], M["col"], M["val"], M["m"], no_transpose=True)
     info = A.info()
@@ -416,92 +369,210 @@ def extras(ff, flush, stream, hbm_peak, args):
         res[f"c4_block_k{k}"] = {"nnz_per_s": info["nnz"] / (ms / 1e3),
                                  "nnz_k_per_s": info["nnz"] * k / (ms / 1e3), "ms": ms,
                                  "alg_gbs": alg / (ms / 1e3) / 1e9,
-                                 "frac": alg / (ms / 1e3) / 1e9 / hbm_peak}
+                                 "frac": alg / (ms / 1e3) / 1e9 / hbm_peak,
+                                 "traffic": ncu_traffic(f"c4_block_k{k}")}
         del X, Y
     del A, M
-    # c5: block Wiedemann sequence, k = ku = 16, m = 65521
+    # c5: block Wiedemann sequence, k = ku = 16, m = 65521 (configs[4]; the
+    # N = 1 point of the N > 1 headline)
+    res["c5_sequence"] = _seq_single(ff, stream, hbm_peak, args)
+    # c5 oracle seconds per step (threaded mode, 2 steps, extrapolated to L)
+    res["c5_sequence"]["cpu_baseline"] = _c5_oracle(oracle, synth)
+    return res
+
+
+def _c5_inputs(synth):
     M = synth.config_matrix("c5")
     n, k = M["rows"], 16
+    g = synth.rng(2005)
+    X = synth.uniform(g, (n, k), M["m"])
+    U = synth.uniform(g, (n, k), M["m"])
+    return M, n, k, X, U
+
+
+def _seq_single(ff, stream, hbm_peak, args):
+    import torch
+
+    import synth
+    M, n, k, X, U = _c5_inputs(synth)
     A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], M["m"], no_transpose=True)
     info = A.info()
-    g = synth.rng(2005)
-    X = to_dev(synth.uniform(g, (n, k), M["m"]))
-    U = to_dev(synth.uniform(g, (n, k), M["m"]))
+    Xd, Ud = to_dev(X), to_dev(U)
     nsteps = 200
     S = torch.empty((nsteps, k, k), dtype=torch.int32, device="cuda")
     ws = torch.empty(ff.ffspmv_workspace_size(A, ff.OP_SEQUENCE, k, k), dtype=torch.uint8, device="cuda")
-    ff.ffspmv_sequence(A, k, X, k, U, 10, S, None, ws, stream)
+    ff.ffspmv_sequence(A, k, Xd, k, Ud, 10, S, None, ws, stream)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ff.ffspmv_kernel_launches()
     e0.record(stream)
-    ff.ffspmv_sequence(A, k, X, k, U, nsteps, S, None, ws, stream)
+    ff.ffspmv_sequence(A, k, Xd, k, Ud, nsteps, S, None, ws, stream)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     L_full = 2 * ((n + k - 1) // k) + 2
-    step_bytes = (info["alg_bytes_apply"] - 4 * 2 * n) + 2 * 2 * k * n + 2 * k * n
-    res["c5_sequence"] = {"steps_per_s": nsteps / (ms / 1e3), "ms_per_step": ms / nsteps,
-                          "steps": nsteps, "L_full": L_full,
-                          "full_L_seconds_extrapolated": L_full * ms / nsteps / 1e3,
-                          "alg_gbs": step_bytes / (ms / nsteps / 1e3) / 1e9,
-                          "frac": step_bytes / (ms / nsteps / 1e3) / 1e9 / hbm_peak,
-                          "launches_per_step": (ff.ffspmv_kernel_launches() - l0) / nsteps,
-                          "note": "L2 not flushed between steps (the iterate is reused by design)"}
-    return res
+    e_v = info["iterate_bytes"]
+    step_bytes = (info["alg_bytes_apply"] - 4 * 2 * n) + 2 * e_v * k * n + e_v * k * n
+    return {"steps_per_s": nsteps / (ms / 1e3), "ms_per_step": ms / nsteps, "steps": nsteps,
+            "L_full": L_full, "full_L_seconds_extrapolated": L_full * ms / nsteps / 1e3,
+            "alg_gbs": step_bytes / (ms / nsteps / 1e3) / 1e9,
+            "frac": step_bytes / (ms / nsteps / 1e3) / 1e9 / hbm_peak,
+            "alg_bytes_per_step": step_bytes,
+            "launches_per_step": (ff.ffspmv_kernel_launches() - l0) / nsteps,
+            "traffic": ncu_traffic("c5_sequence_step"),
+            "note": "one ffspmv_sequence call of 200 steps (S_0..S_199); L2 not flushed between "
+                    "steps (the iterate is reused by design)"}
+
+
+def _c5_oracle(oracle, synth):
+    M, n, k, X, U = _c5_inputs(synth)
+    T = oracle.host_threads()
+    rs, cs, vs = oracle.sort_triples(M["row"], M["col"], M["val"])
+    t0 = time.perf_counter()
+    oracle.sequence_mt(n, rs, cs, vs, M["m"], X, 2, U, nthreads=T)
+    dt = time.perf_counter() - t0
+    L_full = 2 * ((n + k - 1) // k) + 2
+    return {"seconds_per_step": dt / 2, "full_L_seconds_extrapolated": dt / 2 * L_full,
+            "extrapolated": True, "cores": T, "kind": "oracle",
+            "sample": f"2 steps of the full c5 sequence (projection + block apply), threaded "
+                      f"timing mode on {T} threads, extrapolated to L = {L_full}"}
+
+
+# ------------------------------------------------------------- multi-GPU ---
+
+def bench_multi(args, world, rank, local):
+    """N > 1: the c5 sequence as one problem split over the ranks (strong
+    scaling).  steps/s over the timed steps, device events, max over ranks."""
+    r = _seq_dist(args, world, rank, local)
+    hbm_peak, _ = peaks()
+    out = {"metric": METRIC, "value": r.get("steps_per_s"), "unit": "steps/s", "n_gpus": world,
+           "steps": r.get("steps", args.steps), "warmup": args.warmup,
+           "ms_per_step": r.get("ms_per_step"), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "u16 iterate / u32 I/O", "data": "synthetic",
+           "config": {"workload": DESCRIBE["c5"], "rows": 1 << 21, "k": 16, "ku": 16,
+                      "modulus": 65521, "parallelism": r.get("parallelism"),
+                      "l2": "not flushed between steps (the iterate is reused by design)"},
+           "gpu_launches": r.get("launches"), "detail": r}
+    return out
+
+
+def _seq_dist(args, world, rank, local):
+    """c5 sequence across the ranks through dist.sequence_2d on the grid
+    grid_shape picks; timed steps bracketed by device events (on_step hook)."""
+    import torch
+
+    import paper_1004_3719_b200 as ff
+    import synth
+    from paper_1004_3719_b200 import dist as fdist
+    try:
+        M, n, k, X, U = _c5_inputs(synth)
+        steps = max(1, args.steps)
+        L = args.warmup + steps + 1          # the last step only projects
+        pr, pc = fdist.grid_shape(world, k, n=n, nnz=len(M["row"]), iterate_bytes=4)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lc = {}
+
+        def hook(t):
+            if t == args.warmup:
+                torch.cuda.synchronize()
+                torch.distributed.barrier()
+                lc["l0"] = ff.ffspmv_kernel_launches()
+                e0.record()
+            elif t == args.warmup + steps:
+                e1.record()
+                lc["l1"] = ff.ffspmv_kernel_launches()
+                torch.cuda.synchronize()
+
+        fdist.sequence_2d(n, M["row"], M["col"], M["val"], M["m"], X, L, U,
+                          fdist.CudaBackend(f"cuda:{local}"), pr, pc, on_step=hook)
+        ms = e0.elapsed_time(e1)
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+        return {"steps_per_s": steps / (ms / 1e3), "ms_per_step": ms / steps, "steps": steps,
+                "grid": [pr, pc], "launches": lc["l1"] - lc["l0"],
+                "parallelism": f"2-D grid {pr} x {pc} (row bands x column blocks), "
+                               "NCCL all-gather of the iterate per step"}
+    except Exception as e:                       # the line must still print
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 # ------------------------------------------------------------- reference ---
 
 def bench_reference(args):
-    """The oracle arm: same config/metric/unit, CPU, rank 0 only."""
+    """The oracle arm: the headline workload, metric and unit, on the host's
+    cores (threaded timing mode, triples sorted beforehand), rank 0 only."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     import oracle
     import synth
     oracle.build()
-    M = synth.config_matrix(args.config)
-    m, rows, cols = M["m"], M["rows"], M["cols"]
-    g = synth.rng(synth.CONFIGS[args.config]["vseed"])
-    x = synth.uniform(g, cols, m)
-    xt = synth.uniform(g, rows, m)
-    for _ in range(min(args.warmup, 1)):
-        oracle.apply(rows, cols, M["row"], M["col"], M["val"], m, x)
+    T = oracle.host_threads()
+    cfg = HEADLINE if world == 1 else "c5"
+    if cfg == "c5":
+        M, n, k, X, U = _c5_inputs(synth)
+        rs, cs, vs = oracle.sort_triples(M["row"], M["col"], M["val"])
+        step = lambda: oracle.sequence_mt(n, rs, cs, vs, M["m"], X, 1, U, nthreads=T)  # noqa: E731
+        units, unit = 1, "steps/s"
+    else:
+        M = synth.config_matrix(cfg)
+        m, rows, cols = M["m"], M["rows"], M["cols"]
+        g = synth.rng(synth.CONFIGS[cfg]["vseed"])
+        x = synth.uniform(g, cols, m)
+        rs, cs, vs = oracle.sort_triples(M["row"], M["col"], M["val"])
+        step = lambda: oracle.apply_mt(rows, cols, rs, cs, vs, m, x, nthreads=T)  # noqa: E731
+        units, unit = _canonical_nnz(M), "nnz/s"
+    for _ in range(args.warmup):
+        step()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.apply(rows, cols, M["row"], M["col"], M["val"], m, x)
-        oracle.apply_transpose(rows, cols, M["row"], M["col"], M["val"], m, xt)
+        step()
         times.append(time.perf_counter() - t0)
     total = sum(times)
-    nnz = M["row"].size
-    value = 2 * nnz * args.steps / total
-    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
+    value = units * args.steps / total
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": unit, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-           "data": "synthetic",
-           "config": {"workload": f"{args.config}: " + _describe(args.config), "rows": rows,
-                      "cols": cols, "nnz_triples": nnz, "modulus": m},
-           "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": 1, "kind": "oracle",
-                            "sample": f"{args.steps} x (apply + transpose) of the full "
-                                      f"{args.config} matrix", "cpu": _cpu_model()},
-           "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+           "higher_is_better": True, "scaling": "weak" if cfg != "c5" else "strong",
+           "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+           "config": {"workload": DESCRIBE[cfg]},
+           "cpu_baseline": {"value": value, "unit": unit, "cores": T, "kind": "oracle",
+                            "sample": f"{args.steps} steps of the full {cfg} workload (one step = "
+                                      f"{'one sequence step' if cfg == 'c5' else 'y <- A x'}), "
+                                      f"threaded timing mode on {T} threads, after "
+                                      f"{args.warmup} warm-up steps", "cpu": _cpu_model()},
+           "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ main ---
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         bench_reference(args)
     else:

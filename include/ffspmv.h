@@ -77,13 +77,17 @@ enum {
 };
 
 /* Layout of the k = 1 products (apply, apply_transpose).  ROWS: the band
- * formats above, x gathered from L2 per nonzero.  PANELS: A cut into column
- * panels x row bands (the column-wise split of P:290-295); each tile stages
- * its slice of x in shared memory and accumulates its band rows there, then a
- * reduction pass sums the panels (Fig. 2).  AUTO picks PANELS when
- * the columns show little locality (random gathers would be L2-bound).
- * Block apply and the sequence always use ROWS. */
-enum { FFSPMV_STRATEGY_AUTO = 0, FFSPMV_STRATEGY_ROWS = 1, FFSPMV_STRATEGY_PANELS = 2 };
+ * formats above, x gathered from L2 per nonzero.  PANELS and RUNS: A cut
+ * into column panels x row bands (the column-wise split of P:290-295); each
+ * tile stages its slice of x in shared memory and accumulates its band rows
+ * there, and the panels' partial residues are summed per row (Fig. 2,
+ * P:210-222).  PANELS adds every entry into a shared accumulator; RUNS stages
+ * x packed (2/4/8/16/32 bits per residue), sorts each tile by row so a lane
+ * sums runs of one row in registers, and lets the last panel of a band write
+ * y.  AUTO picks RUNS when the columns show little locality (random gathers
+ * would be L2-bound), else ROWS.  Block apply and the sequence use ROWS. */
+enum { FFSPMV_STRATEGY_AUTO = 0, FFSPMV_STRATEGY_ROWS = 1, FFSPMV_STRATEGY_PANELS = 2,
+       FFSPMV_STRATEGY_RUNS = 3 };
 
 /* Operation selectors for ffspmv_apply_host / ffspmv_workspace_size. */
 enum { FFSPMV_OP_APPLY = 0, FFSPMV_OP_TRANSPOSE = 1, FFSPMV_OP_BLOCK = 2, FFSPMV_OP_SEQUENCE = 3,
@@ -111,8 +115,10 @@ typedef struct {
     int32_t check_inputs;    /* 1: apply/sequence verify that x / X / U / y are
                                 canonical (one extra pass + sync per call)       */
     int32_t strategy;        /* apply / apply_transpose layout: FFSPMV_STRATEGY_* */
-    uint32_t panel_rows;     /* PANELS: rows per band, 0 = default (testing)      */
-    uint32_t panel_cols;     /* PANELS: columns per panel, 0 = default (testing)  */
+    uint32_t panel_rows;     /* PANELS / RUNS: rows per band, 0 = default (testing) */
+    uint32_t panel_cols;     /* PANELS / RUNS: columns per panel, 0 = default      */
+    uint32_t panel_xbits;    /* RUNS: bits per staged x residue, 0 = narrowest for
+                                m; 2, 4, 8, 16, 32 (results must not change)     */
 } ffspmv_options;
 
 /* Summary of a built (or analysed) matrix. */
@@ -145,9 +151,10 @@ typedef struct {
     double create_seconds;
     uint32_t strategy_apply;      /* FFSPMV_STRATEGY_ROWS or _PANELS actually used */
     uint32_t strategy_transpose;
-    uint32_t panels, panel_bands; /* P and B of the apply operator (PANELS)       */
-    uint64_t panel_stream_bytes;  /* packed bytes read by one PANELS apply         */
+    uint32_t panels, panel_bands; /* P and B of the apply operator (PANELS / RUNS) */
+    uint64_t panel_stream_bytes;  /* packed bytes read by one PANELS / RUNS apply  */
     double gather_locality;       /* distinct 128 B x lines / nonzeros (sampled)   */
+    uint32_t panel_xbits;         /* bits per staged x residue (PANELS / RUNS)     */
 } ffspmv_info;
 
 /* --- lifecycle ------------------------------------------------------------ */

@@ -32,6 +32,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 typedef unsigned __int128 u128;
 
@@ -186,5 +189,126 @@ int oracle_sequence(uint64_t n, uint64_t nnz,
     return 0;
 }
 
+/* ------------------------------------------------------------------------
+ * Threaded timing mode (used ONLY to time the oracle
+ * on the host's cores for bench.py's cpu_baseline / --impl reference, and
+ * pinned against the serial functions above by tests/test_oracle_pins.py).
+ *
+ * Same definition, same u128 accumulate-then-reduce: the caller passes the
+ * triples sorted by their OUTPUT index `key` (the row for A x, the column for
+ * A^T x) -- sorting is done outside the timed region -- and the triple list
+ * is cut into nthreads contiguous ranges whose boundaries are moved to key
+ * changes, so every output accumulator is owned by exactly one thread: no
+ * races, no change to any sum.  `src` is the other index (the one x is read
+ * at).
+ * ------------------------------------------------------------------------ */
+
+/* thread t's triple range [*lo, *hi): the t-th nnz/T slice, both ends moved
+ * forward to the first triple of a new key */
+static void mt_range(const uint32_t *key, uint64_t nnz, int t, int T, uint64_t *lo, uint64_t *hi)
+{
+    uint64_t a = nnz * (uint64_t)t / (uint64_t)T, b = nnz * (uint64_t)(t + 1) / (uint64_t)T;
+    while (a > 0 && a < nnz && key[a] == key[a - 1]) ++a;
+    while (b > 0 && b < nnz && key[b] == key[b - 1]) ++b;
+    *lo = a;
+    *hi = b < a ? a : b;
+}
+
+static int check_sorted(const uint32_t *key, uint64_t nnz)
+{
+    for (uint64_t t = 1; t < nnz; ++t)
+        if (key[t] < key[t - 1]) return -1;
+    return 0;
+}
+
+/* y[key] <- alpha * sum A x + beta * y over nout outputs, k vectors:
+ * X is nin x k (ldx = k), Y is nout x k (ldy = k). */
+int oracle_apply_sorted_mt(uint64_t nout, uint64_t nin, uint64_t nnz,
+                           const uint32_t *key, const uint32_t *src, const int64_t *val,
+                           uint32_t m, uint32_t k, uint32_t alpha, const uint32_t *X,
+                           uint32_t beta, uint32_t *Y, int nthreads)
+{
+    if (m < 2 || k == 0 || nthreads < 1) return -1;
+    if (check_triples(nout, nin, nnz, key, src) || check_sorted(key, nnz)) return -1;
+    if (check_canonical(X, nin * (uint64_t)k, m)) return -1;
+    if (beta % m && check_canonical(Y, nout * (uint64_t)k, m)) return -1;
+    u128 *acc = (u128 *)calloc(nout * (uint64_t)k + 1, sizeof(u128));
+    if (!acc) return -1;
+    #pragma omp parallel num_threads(nthreads)
+    {
+        int t = 0, T = 1;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+        T = omp_get_num_threads();
+#endif
+        uint64_t lo, hi;
+        mt_range(key, nnz, t, T, &lo, &hi);
+        for (uint64_t e = lo; e < hi; ++e) {
+            uint64_t a = residue(val[e], m);
+            for (uint32_t c = 0; c < k; ++c)
+                acc[(uint64_t)key[e] * k + c] += (u128)a * (u128)X[(uint64_t)src[e] * k + c];
+        }
+        #pragma omp barrier
+        for (uint64_t i = nout * (uint64_t)t / (uint64_t)T; i < nout * (uint64_t)(t + 1) / (uint64_t)T; ++i)
+            for (uint32_t c = 0; c < k; ++c) {
+                uint32_t yold = (beta % m) ? Y[i * k + c] : 0u;
+                Y[i * k + c] = combine(acc[i * k + c], alpha, yold, beta, m);
+            }
+    }
+    free(acc);
+    return 0;
+}
+
+/* The sequence of oracle_sequence with the block apply above (triples
+ * sorted by row) and the projection S_t = U^T V_t summed over nthreads row
+ * ranges (per-thread u128 partial sums, added in thread order, reduced once). */
+int oracle_sequence_mt(uint64_t n, uint64_t nnz,
+                       const uint32_t *ri, const uint32_t *ci, const int64_t *val,
+                       uint32_t m, uint32_t k, const uint32_t *X,
+                       uint32_t ku, const uint32_t *U,
+                       uint64_t L, uint32_t *S, uint32_t *V_out, int nthreads)
+{
+    if (m < 2 || k == 0 || nthreads < 1) return -1;
+    if (U == NULL) { U = X; if (ku != k) return -1; }
+    if (ku == 0) return -1;
+    if (check_triples(n, n, nnz, ri, ci) || check_sorted(ri, nnz)) return -1;
+    if (check_canonical(X, n * (uint64_t)k, m)) return -1;
+    if (check_canonical(U, n * (uint64_t)ku, m)) return -1;
+    uint32_t *V = (uint32_t *)malloc((n * (uint64_t)k + 1) * sizeof(uint32_t));
+    uint32_t *W = (uint32_t *)malloc((n * (uint64_t)k + 1) * sizeof(uint32_t));
+    u128 *part = (u128 *)calloc((uint64_t)nthreads * ku * k + 1, sizeof(u128));
+    if (!V || !W || !part) { free(V); free(W); free(part); return -1; }
+    memcpy(V, X, n * (uint64_t)k * sizeof(uint32_t));
+    for (uint64_t t = 0; t < L; ++t) {
+        memset(part, 0, (uint64_t)nthreads * ku * k * sizeof(u128));
+        #pragma omp parallel num_threads(nthreads)
+        {
+            int th = 0, T = 1;
+#ifdef _OPENMP
+            th = omp_get_thread_num();
+            T = omp_get_num_threads();
+#endif
+            u128 *p = part + (uint64_t)th * ku * k;
+            for (uint64_t r = n * (uint64_t)th / (uint64_t)T; r < n * (uint64_t)(th + 1) / (uint64_t)T; ++r)
+                for (uint32_t a = 0; a < ku; ++a)
+                    for (uint32_t b = 0; b < k; ++b)
+                        p[(uint64_t)a * k + b] += (u128)U[r * ku + a] * (u128)V[r * k + b];
+        }
+        for (uint32_t a = 0; a < ku; ++a)
+            for (uint32_t b = 0; b < k; ++b) {
+                u128 s = 0;
+                for (int th = 0; th < nthreads; ++th) s += part[((uint64_t)th * ku + a) * k + b];
+                S[(t * ku + a) * (uint64_t)k + b] = (uint32_t)(s % m);
+            }
+        if (oracle_apply_sorted_mt(n, n, nnz, ri, ci, val, m, k, 1u, V, 0u, W, nthreads)) {
+            free(V); free(W); free(part); return -1;
+        }
+        uint32_t *tmp = V; V = W; W = tmp;
+    }
+    if (V_out) memcpy(V_out, V, n * (uint64_t)k * sizeof(uint32_t));
+    free(V); free(W); free(part);
+    return 0;
+}
+
 /* Version tag so a stale build is detectable. */
-int oracle_version(void) { return 1; }
+int oracle_version(void) { return 2; }

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libffspmv.so")
 OK, ERR_INVALID_ARG, ERR_MODULUS, ERR_INDEX, ERR_DIM, ERR_NONSQUARE, ERR_UNSUPPORTED, \
     ERR_NOMEM, ERR_CUDA, ERR_NCCL = range(10)
 FMT_AUTO, FMT_SELL, FMT_CSR, FMT_COOS = range(4)
-STRATEGY_AUTO, STRATEGY_ROWS, STRATEGY_PANELS = range(3)
+STRATEGY_AUTO, STRATEGY_ROWS, STRATEGY_PANELS, STRATEGY_RUNS = range(4)
 OP_APPLY, OP_TRANSPOSE, OP_BLOCK, OP_SEQUENCE, OP_PROJECT = range(5)
 
 # Every symbol include/ffspmv.h declares (checked by tests/test_abi.py).
@@ -47,6 +47,7 @@ class ffspmv_options(ctypes.Structure):
         ("strategy", ctypes.c_int32),
         ("panel_rows", ctypes.c_uint32),
         ("panel_cols", ctypes.c_uint32),
+        ("panel_xbits", ctypes.c_uint32),
     ]
 
 
@@ -87,6 +88,7 @@ class ffspmv_info(ctypes.Structure):
         ("panel_bands", ctypes.c_uint32),
         ("panel_stream_bytes", ctypes.c_uint64),
         ("gather_locality", ctypes.c_double),
+        ("panel_xbits", ctypes.c_uint32),
     ]
 
 
@@ -165,7 +167,7 @@ def _check(rc):
 
 def make_options(device=-1, no_transpose=False, segregate_pm1=0, force_format=FMT_AUTO,
                  band_rows=0, long_row=0, force_acc_bits=0, check_inputs=False,
-                 strategy=STRATEGY_AUTO, panel_rows=0, panel_cols=0):
+                 strategy=STRATEGY_AUTO, panel_rows=0, panel_cols=0, panel_xbits=0):
     o = ffspmv_options()
     o.struct_size = ctypes.sizeof(ffspmv_options)
     o.device = device
@@ -179,6 +181,7 @@ def make_options(device=-1, no_transpose=False, segregate_pm1=0, force_format=FM
     o.strategy = strategy
     o.panel_rows = panel_rows
     o.panel_cols = panel_cols
+    o.panel_xbits = panel_xbits
     return o
 
 

@@ -62,6 +62,9 @@ struct ffspmv_matrix_s {
     DevPanel pan[2]{};     // 0 = A, 1 = A^T: panel layout (k = 1 products)
     bool has_pan[2] = {false, false};
     DevMem pmem[2];
+    DevRuns run[2]{};      // 0 = A, 1 = A^T: runs layout (k = 1 products)
+    bool has_run[2] = {false, false};
+    DevMem rmem[2];
     ffspmv_info info{};
     uint32_t *flag = nullptr;          // checked-mode flag (device)
     uint32_t *stage = nullptr;         // apply_host staging (device)
@@ -173,6 +176,47 @@ ffspmv_status upload_panel(const HostPanel &h, DevPanel &d, DevMem &mem) {
     return FFSPMV_OK;
 }
 
+ffspmv_status upload_runs(const HostRuns &h, DevRuns &d, DevMem &mem) {
+    struct Part { const void *src; size_t bytes; void **dst; };
+    d = DevRuns{};
+    d.rows = h.rows;
+    d.cols = h.cols;
+    d.g = h.g;
+    void *p_tiles, *p_words, *p_vval, *p_cta, *p_part, *p_xp;
+    Part parts[] = {
+        {h.tiles.data(), h.tiles.size() * sizeof(RunsTile), &p_tiles},
+        {h.words.data(), h.words.size() * 4, &p_words},
+        {h.vval.data(), h.vval.size(), &p_vval},
+        {h.cta_t0.data(), h.cta_t0.size() * 4, &p_cta},
+        {nullptr, (size_t)h.g.P * h.g.rows_pad * h.g.pbytes, &p_part},
+        {nullptr, (size_t)h.g.P * h.g.panel_bytes, &p_xp},
+    };
+    size_t total = 0;
+    for (auto &pt : parts) total += a256(pt.bytes);
+    total = std::max<size_t>(total, 256);
+    int e = cudaMalloc(&mem.base, total);
+    if (e) return e == cudaErrorMemoryAllocation ? fail(FFSPMV_ERR_NOMEM, "cudaMalloc of runs")
+                                                 : cuda_fail(e, "cudaMalloc");
+    mem.bytes = total;
+    size_t off = 0;
+    for (auto &pt : parts) {
+        *pt.dst = (char *)mem.base + off;
+        if (pt.bytes) {
+            e = pt.src ? cudaMemcpy(*pt.dst, pt.src, pt.bytes, cudaMemcpyHostToDevice)
+                       : cudaMemset(*pt.dst, 0, pt.bytes);
+            if (e) { cudaFree(mem.base); mem.base = nullptr; return cuda_fail(e, "runs upload"); }
+        }
+        off += a256(pt.bytes);
+    }
+    d.tiles = (const RunsTile *)p_tiles;
+    d.words = (const uint32_t *)p_words;
+    d.vval = p_vval;
+    d.cta_t0 = (const uint32_t *)p_cta;
+    d.partial = p_part;
+    d.xpack = p_xp;
+    return FFSPMV_OK;
+}
+
 ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &device, bool &want_t,
                            bool &checked) {
     device = -1;
@@ -203,16 +247,24 @@ ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &devic
         return fail(FFSPMV_ERR_INVALID_ARG, "force_acc_bits must be 0, 32, 64 or 96");
     bo.force_acc_bits = o->force_acc_bits;
     if (o->struct_size >= sizeof(ffspmv_options)) {
-        if (o->strategy < 0 || o->strategy > 2)
-            return fail(FFSPMV_ERR_INVALID_ARG, "strategy must be 0, 1 or 2");
+        if (o->strategy < 0 || o->strategy > 3)
+            return fail(FFSPMV_ERR_INVALID_ARG, "strategy must be 0, 1, 2 or 3");
         bo.strategy = o->strategy;
-        if (o->panel_rows && (o->panel_rows > 32768 || o->panel_rows % 32))
+        if (o->strategy != 3 && o->panel_rows && (o->panel_rows > 32768 || o->panel_rows % 32))
             return fail(FFSPMV_ERR_INVALID_ARG, "panel_rows must be a multiple of 32 <= 32768");
         if (o->panel_cols && (o->panel_cols > 262144 || o->panel_cols % 32))
             return fail(FFSPMV_ERR_INVALID_ARG, "panel_cols must be a multiple of 32 <= 262144");
         bo.panel_rows = o->panel_rows;
         bo.panel_cols = o->panel_cols;
     }
+    if (o->struct_size >= offsetof(ffspmv_options, panel_xbits) + sizeof(o->panel_xbits)) {
+        if (o->panel_xbits && o->panel_xbits != 2 && o->panel_xbits != 4 && o->panel_xbits != 8 &&
+            o->panel_xbits != 16 && o->panel_xbits != 32)
+            return fail(FFSPMV_ERR_INVALID_ARG, "panel_xbits must be 0, 2, 4, 8, 16 or 32");
+        bo.xbits = o->panel_xbits;
+    }
+    if (bo.strategy == 3 && bo.panel_rows && (bo.panel_rows % 4 || bo.panel_rows > 16384))
+        return fail(FFSPMV_ERR_INVALID_ARG, "runs: panel_rows must be a multiple of 4 <= 16384");
     return FFSPMV_OK;
 }
 
@@ -229,8 +281,10 @@ ffspmv_status check_triples_args(uint64_t rows, uint64_t cols, uint64_t nnz, con
 struct Built {
     HostOp rows[2];
     HostPanel pan[2];
+    HostRuns run[2];
     bool has_rows[2] = {false, false};
     bool has_pan[2] = {false, false};
+    bool has_run[2] = {false, false};
     double locality = 0;
 };
 
@@ -261,26 +315,66 @@ void fill_stats(ffspmv_info &I, const Built &b, uint32_t m) {
     I.stream_bytes = a.stream_bytes;
     uint64_t vb = I.value_bytes;
     I.alg_bytes_apply = 4 * a.nnz_pm + (4 + vb) * a.nnz_val + 4ull * a.cols + 4ull * a.rows;
-    bool has_t = b.has_rows[1] || b.has_pan[1];
+    bool has_t = b.has_rows[1] || b.has_pan[1] || b.has_run[1];
     if (has_t)
         I.alg_bytes_transpose = 4 * a.nnz_pm + (4 + vb) * a.nnz_val + 4ull * a.cols + 4ull * a.rows;
     I.has_transpose = has_t;
-    I.strategy_apply = b.has_pan[0] ? FFSPMV_STRATEGY_PANELS : FFSPMV_STRATEGY_ROWS;
-    I.strategy_transpose = !has_t ? 0 : b.has_pan[1] ? FFSPMV_STRATEGY_PANELS : FFSPMV_STRATEGY_ROWS;
-    if (b.has_pan[0]) {
+    auto strat = [&](int k) {
+        return b.has_run[k] ? FFSPMV_STRATEGY_RUNS : b.has_pan[k] ? FFSPMV_STRATEGY_PANELS
+                                                                  : FFSPMV_STRATEGY_ROWS;
+    };
+    I.strategy_apply = strat(0);
+    I.strategy_transpose = !has_t ? 0 : strat(1);
+    if (b.has_run[0]) {
+        I.panels = b.run[0].g.P;
+        I.panel_bands = b.run[0].g.B;
+        I.panel_stream_bytes = b.run[0].stream_bytes;
+        I.panel_xbits = b.run[0].g.xbits;
+    } else if (b.has_pan[0]) {
         I.panels = b.pan[0].g.P;
         I.panel_bands = b.pan[0].g.B;
         I.panel_stream_bytes = b.pan[0].stream_bytes;
+        I.panel_xbits = 8 * b.pan[0].g.xbytes;
     }
     I.gather_locality = b.locality;
 }
 
-bool choose_panels(const Canon &c, uint32_t m, const BuildOptions &bo, uint32_t nsm, double loc) {
-    if (bo.strategy == FFSPMV_STRATEGY_ROWS) return false;
+// random columns (little 128 B line reuse) and enough work to fill the SMs:
+// x is better staged in shared memory than gathered from L2
+bool x_staged(const Canon &c, double loc) { return loc > 0.5 && c.idx.size() >= (1u << 20); }
+
+// PANELS (x staged in shared memory, one shared atomic per entry): the
+// default for staged x wider than a byte (m > 256)
+bool choose_panels(const Canon &c, uint32_t m, const BuildOptions &bo, double loc) {
     if (bo.strategy == FFSPMV_STRATEGY_PANELS) return true;
-    PanelGeom g = panel_geometry(c.nrows, c.ncols, m, bo, nsm);
-    // random columns (little line reuse) + enough tiles to fill the SMs
-    return loc > 0.5 && (uint64_t)g.P * g.B >= nsm && c.idx.size() >= (1u << 20);
+    return bo.strategy == FFSPMV_STRATEGY_AUTO && m > 256u && x_staged(c, loc);
+}
+
+// RUNS (x staged packed in shared memory, register row runs): the default
+// for m <= 256, where x packs to 2-8 bits and few panels cover the columns
+bool choose_runs(const Canon &c, uint32_t m, const BuildOptions &bo, double loc) {
+    if (bo.strategy == FFSPMV_STRATEGY_RUNS) return true;
+    return bo.strategy == FFSPMV_STRATEGY_AUTO && m <= 256u && x_staged(c, loc);
+}
+
+// the k = 1 layout of one operator (A or A^T): RUNS, PANELS or ROWS
+void pack_k1(Built &out, int k, const Canon &c, uint32_t m, const BuildOptions &bo, uint32_t nsm,
+             double loc, bool need_rows) {
+    if (choose_runs(c, m, bo, loc) && pack_runs(out.run[k], c, m, bo, nsm)) {
+        out.has_run[k] = true;
+    } else {
+        out.run[k] = HostRuns();
+        if (choose_panels(c, m, bo, loc) && pack_panels(out.pan[k], c, m, bo, nsm)) {
+            out.has_pan[k] = true;
+        } else {
+            out.pan[k] = HostPanel();
+            need_rows = true;
+        }
+    }
+    if (need_rows && !out.has_rows[k]) {
+        pack_operator(out.rows[k], c, m, bo);
+        out.has_rows[k] = true;
+    }
 }
 
 ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t *ri,
@@ -297,29 +391,20 @@ ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint3
     if (rc) return fail((ffspmv_status)rc, err);
     try {
         out.locality = gather_locality(ca);
-        pack_operator(out.rows[0], ca, m, bo);   // block apply + sequence always use rows
-        out.has_rows[0] = true;
-        if (choose_panels(ca, m, bo, nsm, out.locality))
-            out.has_pan[0] = pack_panels(out.pan[0], ca, m, bo, nsm);
+        // block apply + sequence always use the rows layout of A
+        pack_k1(out, 0, ca, m, bo, nsm, out.locality, true);
         if (want_t) {
             Canon ct;
             transpose_canon(ct, ca);
             ca = Canon();
-            if (choose_panels(ct, m, bo, nsm, gather_locality(ct)) &&
-                pack_panels(out.pan[1], ct, m, bo, nsm)) {
-                out.has_pan[1] = true;
-            } else {
-                out.pan[1] = HostPanel();
-                pack_operator(out.rows[1], ct, m, bo);
-                out.has_rows[1] = true;
-            }
+            pack_k1(out, 1, ct, m, bo, nsm, gather_locality(ct), false);
         }
     } catch (const std::bad_alloc &) {
         return fail(FFSPMV_ERR_NOMEM, "host allocation during packing");
     }
     for (int k = 0; k < 2; ++k)
         if (out.rows[k].pcol.size() >= (1ull << 32) || out.rows[k].vcol.size() >= (1ull << 32) ||
-            out.pan[k].pent.size() >= (1ull << 32))
+            out.pan[k].pent.size() >= (1ull << 32) || out.run[k].words.size() >= (1ull << 32))
             return fail(FFSPMV_ERR_DIM, "packed streams exceed 2^32 slots");
     return FFSPMV_OK;
 }
@@ -369,6 +454,7 @@ ffspmv_status ffspmv_create(ffspmv_matrix *out, uint64_t rows, uint64_t cols, ui
         for (int k = 0; k < 2; ++k) {
             if (h->mem[k].base) cudaFree(h->mem[k].base);
             if (h->pmem[k].base) cudaFree(h->pmem[k].base);
+            if (h->rmem[k].base) cudaFree(h->rmem[k].base);
         }
         if (h->flag) cudaFree(h->flag);
         delete h;
@@ -382,6 +468,10 @@ ffspmv_status ffspmv_create(ffspmv_matrix *out, uint64_t rows, uint64_t cols, ui
             if ((s = upload_panel(B.pan[k], h->pan[k], h->pmem[k]))) { cleanup(); return s; }
             h->has_pan[k] = true;
         }
+        if (B.has_run[k]) {
+            if ((s = upload_runs(B.run[k], h->run[k], h->rmem[k]))) { cleanup(); return s; }
+            h->has_run[k] = true;
+        }
     }
     if ((e = cudaMalloc((void **)&h->flag, 256))) {
         cleanup();
@@ -389,7 +479,8 @@ ffspmv_status ffspmv_create(ffspmv_matrix *out, uint64_t rows, uint64_t cols, ui
     }
     fill_stats(h->info, B, modulus);
     h->info.nnz_input = nnz;
-    h->info.device_bytes = h->mem[0].bytes + h->mem[1].bytes + h->pmem[0].bytes + h->pmem[1].bytes + 256;
+    h->info.device_bytes = h->mem[0].bytes + h->mem[1].bytes + h->pmem[0].bytes + h->pmem[1].bytes +
+                           h->rmem[0].bytes + h->rmem[1].bytes + 256;
     h->info.create_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     h->checked = checked;
@@ -403,6 +494,8 @@ ffspmv_status ffspmv_destroy(ffspmv_matrix A) {
     for (auto &mem : A->mem)
         if (mem.base) cudaFree(mem.base);
     for (auto &mem : A->pmem)
+        if (mem.base) cudaFree(mem.base);
+    for (auto &mem : A->rmem)
         if (mem.base) cudaFree(mem.base);
     if (A->flag) cudaFree(A->flag);
     if (A->stage) cudaFree(A->stage);
@@ -444,11 +537,10 @@ ffspmv_status ffspmv_analyze(uint64_t rows, uint64_t cols, uint64_t nnz, const u
         if (!rec_row || !rec_col || !rec_val || !rec_n)
             return fail(FFSPMV_ERR_INVALID_ARG, "reconstruction needs all of rec_row/col/val/n");
         const int k = transpose ? 1 : 0;
-        uint64_t n = B.has_pan[k]
-                         ? reconstruct_panels(B.pan[k], modulus, value_bytes_for(modulus), rec_row,
-                                              rec_col, rec_val, rec_cap)
-                         : reconstruct(B.rows[k], modulus, value_bytes_for(modulus), rec_row,
-                                       rec_col, rec_val, rec_cap);
+        const uint32_t vb = value_bytes_for(modulus);
+        uint64_t n = B.has_run[k]   ? reconstruct_runs(B.run[k], modulus, vb, rec_row, rec_col, rec_val, rec_cap)
+                     : B.has_pan[k] ? reconstruct_panels(B.pan[k], modulus, vb, rec_row, rec_col, rec_val, rec_cap)
+                                    : reconstruct(B.rows[k], modulus, vb, rec_row, rec_col, rec_val, rec_cap);
         *rec_n = n;
         if (n > rec_cap) return fail(FFSPMV_ERR_NOMEM, "reconstruction capacity too small");
     }
@@ -458,6 +550,12 @@ ffspmv_status ffspmv_analyze(uint64_t rows, uint64_t cols, uint64_t nnz, const u
 }  // extern "C"
 
 namespace {
+
+void op_dims(ffspmv_matrix A, int which, uint64_t &rows, uint64_t &cols) {
+    if (A->has_run[which]) { rows = A->run[which].rows; cols = A->run[which].cols; }
+    else if (A->has_pan[which]) { rows = A->pan[which].rows; cols = A->pan[which].cols; }
+    else { rows = A->op[which].rows; cols = A->op[which].cols; }
+}
 
 ffspmv_status check_vec(ffspmv_matrix A, const uint32_t *v, uint64_t n, uint64_t ld, uint64_t w,
                         void *stream, const char *name) {
@@ -475,10 +573,10 @@ ffspmv_status check_vec(ffspmv_matrix A, const uint32_t *v, uint64_t n, uint64_t
 ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_t *x, uint64_t nx,
                        uint32_t beta, uint32_t *y, uint64_t ny, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
-    if (!A->has_op[which] && !A->has_pan[which])
+    if (!A->has_op[which] && !A->has_pan[which] && !A->has_run[which])
         return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built (no_transpose was set)");
-    const uint64_t orows = A->has_pan[which] ? A->pan[which].rows : A->op[which].rows;
-    const uint64_t ocols = A->has_pan[which] ? A->pan[which].cols : A->op[which].cols;
+    uint64_t orows, ocols;
+    op_dims(A, which, orows, ocols);
     if (nx != ocols || ny != orows)
         return fail(FFSPMV_ERR_DIM, "x must have " + std::to_string(ocols) + " and y " +
                                         std::to_string(orows) + " entries");
@@ -490,8 +588,9 @@ ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_
     ffspmv_status s;
     if ((s = check_vec(A, x, nx, 1, 1, stream, "x"))) return s;
     if (beta && (s = check_vec(A, y, ny, 1, 1, stream, "y"))) return s;
-    int e = A->has_pan[which] ? launch_panel_apply(A->pan[which], A->mod, alpha, x, beta, y, stream)
-                              : launch_apply(A->op[which], A->mod, alpha, x, beta, y, stream);
+    int e = A->has_run[which]   ? launch_runs_apply(A->run[which], A->mod, alpha, x, beta, y, stream)
+            : A->has_pan[which] ? launch_panel_apply(A->pan[which], A->mod, alpha, x, beta, y, stream)
+                                : launch_apply(A->op[which], A->mod, alpha, x, beta, y, stream);
     if (e) return cuda_fail(e, "apply launch");
     return FFSPMV_OK;
 }
@@ -539,10 +638,10 @@ ffspmv_status ffspmv_apply_host(ffspmv_matrix A, int which, uint32_t alpha, cons
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
     if (which != FFSPMV_OP_APPLY && which != FFSPMV_OP_TRANSPOSE)
         return fail(FFSPMV_ERR_INVALID_ARG, "op must be FFSPMV_OP_APPLY or FFSPMV_OP_TRANSPOSE");
-    if (!A->has_op[which] && !A->has_pan[which])
+    if (!A->has_op[which] && !A->has_pan[which] && !A->has_run[which])
         return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built");
-    struct { uint64_t rows, cols; } op{A->has_pan[which] ? A->pan[which].rows : A->op[which].rows,
-                                       A->has_pan[which] ? A->pan[which].cols : A->op[which].cols};
+    struct { uint64_t rows, cols; } op{};
+    op_dims(A, which, op.rows, op.cols);
     if ((op.cols && !x_host) || (op.rows && !y_host))
         return fail(FFSPMV_ERR_INVALID_ARG, "NULL host vector");
     std::lock_guard<std::mutex> lk(A->mu);
@@ -578,7 +677,7 @@ ffspmv_status ffspmv_workspace_size(ffspmv_matrix A, int which, uint32_t k, uint
     if (which == FFSPMV_OP_PROJECT) {
         if (k == 0 || ku == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k and ku must be >= 1");
         DeviceGuard guard(A->device);
-        *bytes = project_workspace(A->has_op[0] ? A->op[0].rows : A->pan[0].rows, k, ku);
+        *bytes = project_workspace(A->op[0].rows, k, ku);
         return FFSPMV_OK;
     }
     if (which != FFSPMV_OP_SEQUENCE) { *bytes = 0; return FFSPMV_OK; }
@@ -603,6 +702,9 @@ ffspmv_status ffspmv_sequence(ffspmv_matrix A, uint32_t k, const uint32_t *X, ui
         return fail(FFSPMV_ERR_INVALID_ARG, "ku must be >= 1");
     }
     const uint64_t n = op.rows;
+    // the step kernels index the iterate with 32-bit element offsets
+    if (n * k >= (1ull << 32) || n * ku >= (1ull << 32))
+        return fail(FFSPMV_ERR_DIM, "n * k and n * ku must be < 2^32 elements");
     if (n && !X) return fail(FFSPMV_ERR_INVALID_ARG, "NULL X");
     if (L && !S) return fail(FFSPMV_ERR_INVALID_ARG, "NULL S");
     if (overlaps(S, L * ku * k * 4ull, X, n * k * 4ull) ||
@@ -635,7 +737,7 @@ ffspmv_status ffspmv_project(ffspmv_matrix A, uint32_t k, const uint32_t *V, uin
                              size_t workspace_bytes, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
     if (k == 0 || ku == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k and ku must be >= 1");
-    const uint64_t n = A->has_op[0] ? A->op[0].rows : A->pan[0].rows;
+    const uint64_t n = A->op[0].rows;
     if ((n && (!V || !U)) || !S) return fail(FFSPMV_ERR_INVALID_ARG, "NULL V, U or S");
     if (overlaps(S, (size_t)ku * k * 4, V, n * k * 4) || overlaps(S, (size_t)ku * k * 4, U, n * ku * 4))
         return fail(FFSPMV_ERR_INVALID_ARG, "S overlaps an input");

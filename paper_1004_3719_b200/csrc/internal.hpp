@@ -120,9 +120,11 @@ struct BuildOptions {
     uint32_t long_row = 512;
     uint32_t split_chunk = 1u << 14;
     int force_acc_bits = 0;
-    int strategy = 0;          // 0 auto, 1 rows (x gathered from L2), 2 panels (x in smem)
+    int strategy = 0;          // 0 auto, 1 rows (x gathered from L2), 2 panels (x in smem),
+                               // 3 runs (packed x in smem, register row runs)
     uint32_t panel_rows = 0;   // 0 = default R (testing: smaller tiles)
     uint32_t panel_cols = 0;   // 0 = default W (testing: smaller panels)
+    uint32_t xbits = 0;        // runs: 0 = narrowest for m; else forced (2/4/8/16/32, >= need)
 };
 
 // ------------------------------------------------------------------ panels --
@@ -193,6 +195,83 @@ uint64_t reconstruct_panels(const HostPanel &hp, uint32_t m, uint32_t vbytes, ui
 double gather_locality(const Canon &a);
 int launch_panel_apply(const DevPanel &op, const DevMod &M, uint32_t alpha, const uint32_t *x,
                        uint32_t beta, uint32_t *y, void *stream);
+
+// -------------------------------------------------------------------- runs --
+// Second 2-D tiled operator for k = 1 (FFSPMV_STRATEGY_RUNS).  Same tiling
+// idea as PANELS (the column-wise split of P:290-295: column panel p x row
+// band, x panel staged in shared memory, one residue per band row per panel
+// summed by a reduction pass, Fig. 2), but:
+//   * the x panel is staged PACKED (xbits = 2 / 4 / 8 / 16 / 32 bits per
+//     residue): a pre-pass packs x once per call and each CTA copies its
+//     panel with bulk-async copies;
+//   * a unit (panel p x an R-row band, unit u = p * B + b) holds three
+//     sections, +1, -1 and valued entries, each sorted by row and
+//     cut into chunks of 32 lanes x RUN_E consecutive entries, so a lane sums
+//     a run of one row in a register and touches shared memory only when its
+//     row changes;
+//   * every warp owns private band accumulators and takes whole units, so no
+//     CTA barrier separates units.
+//
+// Entry word: byte offset of the 32-bit word of the staged panel holding the
+// column's residue in bits [5 + rs, 32), the band row in bits [5, 5 + rs), the
+// residue's bit offset inside that word in bits [0, 5).  Chunk c of a section
+// holds entries [512 c, 512 c + 512) (RUN_E = 16): entry 16 l + j goes to
+// lane l, slot j, at word 512 c + 128 (j / 4) + 4 l + (j % 4) (four coalesced
+// 16-byte loads per lane) and, for values, at 512 c + 16 l + j.  Padding
+// entries point at the zero word past the panel (byte offset panel_bytes).
+constexpr uint32_t RUN_E = 16;
+constexpr uint32_t RUN_CHUNK = 32 * RUN_E;
+constexpr uint32_t RUN_WARPS = 16;    // warps per k_runs CTA, each with private band accumulators
+
+struct RunsGeom {
+    uint32_t W = 0, R = 0, P = 0, B = 0;
+    uint32_t xbits = 32;       // bits per staged x residue (2, 4, 8, 16, 32)
+    uint32_t wide = 0;         // 1: m > 2^16 (u64 run sums, split u32 band accumulators)
+    uint32_t pbytes = 4;       // bytes per partial residue (1, 2, 4)
+    uint32_t rs = 9;           // row bits of the entry word (R <= 2^rs)
+    uint32_t nctas = 0;        // persistent CTAs (one per SM)
+    uint32_t panel_bytes = 0;  // bytes of one packed x panel (multiple of 16)
+    uint32_t rows_pad = 0;     // partial row stride (rows rounded up to 16)
+};
+
+// One unit: chunks [c0, c0 + npc) of +1 entries, the next nmc chunks of -1
+// entries, the next nvc chunks of valued entries whose values are value
+// chunks [vc0, vc0 + nvc); rn: live band rows.  Units are panel-major: unit
+// u covers panel u / B and band u % B.
+struct RunsTile {
+    uint32_t c0, npc, nmc, nvc, vc0, rn, pad0, pad1;
+};
+static_assert(sizeof(RunsTile) == 32, "RunsTile is 32 bytes");
+
+struct HostRuns {
+    uint32_t rows = 0, cols = 0;
+    RunsGeom g;
+    std::vector<RunsTile> tiles;       // P*B tiles, panel-major
+    std::vector<uint32_t> words;       // RUN_CHUNK words per chunk
+    std::vector<uint8_t> vval;         // RUN_CHUNK values (vbytes each) per value chunk
+    std::vector<uint32_t> cta_t0;      // nctas + 1 tile boundaries
+    uint64_t nnz_pm = 0, nnz_val = 0, stream_bytes = 0;
+};
+
+struct DevRuns {
+    uint32_t rows, cols;
+    RunsGeom g;
+    const RunsTile *tiles;
+    const uint32_t *words, *cta_t0;
+    const void *vval;
+    void *partial;                     // P * rows_pad * pbytes scratch
+    void *xpack;                       // P * panel_bytes scratch (packed x)
+};
+
+RunsGeom runs_geometry(uint64_t rows, uint64_t cols, uint64_t nnz, uint32_t m,
+                       const BuildOptions &bo, uint32_t nsm);
+// false when a band row's u32 accumulator could overflow (m <= 2^16; the
+// caller then keeps another layout)
+bool pack_runs(HostRuns &hr, const Canon &a, uint32_t m, const BuildOptions &bo, uint32_t nsm);
+uint64_t reconstruct_runs(const HostRuns &hr, uint32_t m, uint32_t vbytes, uint32_t *rr,
+                          uint32_t *rc, uint32_t *rv, uint64_t cap);
+int launch_runs_apply(const DevRuns &op, const DevMod &M, uint32_t alpha, const uint32_t *x,
+                      uint32_t beta, uint32_t *y, void *stream);
 
 // Canonical CSR: rows sorted by column, duplicates summed mod m, zeros dropped.
 struct Canon {

@@ -307,7 +307,12 @@ SeqLayout<IT> layout(void *ws, const DevOp &op, uint32_t m, uint32_t k, uint32_t
     size_t off = 0;
     const bool mma = sizeof(IT) == 2 && mma_ok(m, k, ku);
     const uint32_t ucols = mma ? 0 : fused_ok(k, ku) ? kup_for(ku) : ku;
-    const uint32_t maxc = std::max<uint32_t>(nctas, (uint32_t)num_sms() * MAX_STEP_CTAS_PER_SM);
+    // fused steps ping-pong two partial buffers of up to maxc CTA rows (the
+    // step kernels' grid, or the projection's for S_0); the unfused path
+    // only uses partial[0] with the projection's nctas rows
+    const bool fused = mma || fused_ok(k, ku);
+    const uint32_t maxc = fused ? std::max<uint32_t>(nctas, (uint32_t)num_sms() * MAX_STEP_CTAS_PER_SM)
+                                : nctas;
     size_t vb = align256(n * (size_t)k * sizeof(IT));
     size_t ub = align256(n * (size_t)ucols * sizeof(IT));
     size_t pb = align256((size_t)maxc * ku * k * sizeof(uint32_t));
@@ -316,7 +321,7 @@ SeqLayout<IT> layout(void *ws, const DevOp &op, uint32_t m, uint32_t k, uint32_t
     L.V[1] = (IT *)(p + off); off += vb;
     L.Uc = (IT *)(p + off); off += ub;
     L.partial[0] = (uint32_t *)(p + off); off += pb;
-    L.partial[1] = (uint32_t *)(p + off); off += pb;
+    L.partial[1] = (uint32_t *)(p + off); off += fused ? pb : 0;
     L.ufrag = (uint32_t *)(p + off); off += fb;
     L.opdev = (DevOp *)(p + off); off += align256(sizeof(DevOp));
     L.bytes = off;
@@ -457,8 +462,9 @@ int launch_step_mma(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32
     // k = 8 / 16: the lean half-slice kernel (16-byte gathers, one row per lane)
     if (k == 8) return launch_step_h_t<VT, 1>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
     if (k == 16) return launch_step_h_t<VT, 2>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
-    if (k <= 4) return launch_step_mma_t<VT, 1, 4>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
-    if (k <= 8) return launch_step_mma_t<VT, 2, 8>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+    // remaining mma_ok widths: k = 4 (one lane per row) and k = 12 (four
+    // 4-column lanes per row, the last one idle)
+    if (k == 4) return launch_step_mma_t<VT, 1, 4>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
     return launch_step_mma_t<VT, 4, 16>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
 }
 

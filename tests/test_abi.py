@@ -68,6 +68,9 @@ OPTION_SETS = [
     dict(force_acc_bits=96), dict(force_acc_bits=64, force_format=3),
     dict(strategy=2), dict(strategy=2, panel_rows=32, panel_cols=32),
     dict(strategy=2, panel_rows=64, panel_cols=96, segregate_pm1=-1),
+    dict(strategy=3), dict(strategy=3, panel_rows=32, panel_cols=64),
+    dict(strategy=3, panel_rows=8, panel_cols=64, segregate_pm1=-1, panel_xbits=32),
+    dict(strategy=3, panel_rows=12, panel_cols=128, panel_xbits=16),
 ]
 
 
@@ -145,6 +148,11 @@ def test_panel_strategy_choice(lib):
     assert info["gather_locality"] > 0.7
     assert info["strategy_apply"] == lib.STRATEGY_PANELS == info["strategy_transpose"]
     assert info["panels"] == 8 and info["panel_bands"] == -(-M["rows"] // 8160)
+    # m = 3: RUNS, x staged at 2 bits: 1024-row units leave 17 offset bits
+    # (128 KB panels, 524224 columns) -> 2 panels
+    info = lib.ffspmv_analyze(M["rows"], M["cols"], M["row"], M["col"], M["val"], 3)
+    assert info["strategy_apply"] == lib.STRATEGY_RUNS and info["panel_xbits"] == 2
+    assert info["panels"] == 2
     # banded matrix: columns local -> rows layout
     n = 1 << 19
     ri = np.repeat(np.arange(n, dtype=np.uint32), 4)

@@ -20,7 +20,10 @@ OPTS = [dict(), dict(force_format=1), dict(force_format=2), dict(force_format=3)
         dict(segregate_pm1=-1), dict(band_rows=32, long_row=6), dict(force_acc_bits=96),
         dict(force_acc_bits=64, force_format=2, long_row=3),
         dict(strategy=2), dict(strategy=2, panel_rows=32, panel_cols=64),
-        dict(strategy=2, panel_rows=96, panel_cols=32, segregate_pm1=-1)]
+        dict(strategy=2, panel_rows=96, panel_cols=32, segregate_pm1=-1),
+        dict(strategy=3), dict(strategy=3, panel_rows=32, panel_cols=64),
+        dict(strategy=3, panel_rows=8, panel_cols=64, segregate_pm1=-1, panel_xbits=32),
+        dict(strategy=3, panel_rows=12, panel_cols=128, panel_xbits=16)]
 
 
 def dev(a):
@@ -121,24 +124,12 @@ def test_sequence_parity(ff, oracle_mod, cuda, m):
         assert np.array_equal(host(V), Vw)
 
 
-def test_sequence_chaining_and_paper_example(ff, oracle_mod, cuda):
+def test_sequence_paper_example(ff, oracle_mod, cuda):
     # P:249-261 example: S_i = 2*3^i mod 27
     A = ff.ffspmv_create(2, 2, np.array([0, 0, 1], np.uint32), np.array([0, 1, 1], np.uint32),
                          np.array([2, 1, 3], np.int64), 27)
     S = A.sequence(dev(np.ones((2, 1), np.uint32)), 5)
     assert host(S).ravel().tolist() == [2, 6, 18, 0, 0]
-    m = 65521
-    g = synth.rng(5)
-    n, k = 300, 4
-    ri, ci, val = synth.random_coo(g, n, n, 2000, m)
-    A = ff.ffspmv_create(n, n, ri, ci, val, m)
-    X = dev(synth.uniform(g, (n, k), m))
-    U = dev(synth.uniform(g, (n, 3), m))
-    S, V = A.sequence(X, 9, U, want_vout=True)
-    S1, V1 = A.sequence(X, 4, U, want_vout=True)
-    S2, V2 = A.sequence(V1, 5, U, want_vout=True)
-    assert np.array_equal(host(S), np.concatenate([host(S1), host(S2)]))
-    assert np.array_equal(host(V), host(V2))
 
 
 def test_empty_and_degenerate(ff, oracle_mod, cuda):
@@ -232,8 +223,9 @@ def test_overflow_adversarial(ff, oracle_mod, cuda):
                                                                   np.array([m - 1, m - 1]), 1, 1))
 
 
+@pytest.mark.parametrize("strategy", [2, 3])
 @pytest.mark.parametrize("m", [251, 65521, 65536])
-def test_panel_overflow_adversarial(ff, oracle_mod, cuda, m):
+def test_panel_overflow_adversarial(ff, oracle_mod, cuda, m, strategy):
     """Panel tiles whose row sums approach 2^32: one dense row per section
     kind (+1, -1 with x = 0, valued m-2 with x = m-1), long enough that the
     lazy Barrett remainders (< 2m) would overflow a u32 and, for m = 65536,
@@ -245,15 +237,16 @@ def test_panel_overflow_adversarial(ff, oracle_mod, cuda, m):
         ci = np.arange(n, dtype=np.uint32)
         val = np.full(n, v, np.int64)
         x = np.full(cols, xv, np.uint32)
-        A = ff.ffspmv_create(3, cols, ri, ci, val, m, strategy=2)
+        A = ff.ffspmv_create(3, cols, ri, ci, val, m, strategy=strategy)
         y0 = np.array([m - 1, 1, 0], np.uint32)
         yd = dev(y0)
         ff.ffspmv_apply(A, 1, dev(x), 1, yd)
         assert np.array_equal(host(yd), oracle_mod.apply(3, cols, ri, ci, val, m, x, y0, 1, 1))
 
 
+@pytest.mark.parametrize("strategy", [2, 3])
 @pytest.mark.parametrize("m", [3, 65521, 65537])
-def test_panel_pipeline_many_tiles(ff, oracle_mod, cuda, m):
+def test_panel_pipeline_many_tiles(ff, oracle_mod, cuda, m, strategy):
     """Panel schedule edge cases: > 64 tiles per CTA (header-cache reloads,
     tiny 32 x 32 tiles) and tiles with more quads than the register ring
     (> 16384 entries in one tile, the overflow loop)."""
@@ -261,8 +254,8 @@ def test_panel_pipeline_many_tiles(ff, oracle_mod, cuda, m):
     for rows, cols, nnz, kw in ((6000, 6000, 60000, dict(panel_rows=32, panel_cols=32)),
                                 (20000, 20000, 120000, dict())):
         ri, ci, val = synth.random_coo(g, rows, cols, nnz, m, dup=0.0, big=True)
-        A = ff.ffspmv_create(rows, cols, ri, ci, val, m, strategy=2, **kw)
-        assert A.info()["strategy_apply"] == ff.STRATEGY_PANELS
+        A = ff.ffspmv_create(rows, cols, ri, ci, val, m, strategy=strategy, **kw)
+        assert A.info()["strategy_apply"] == strategy
         x = synth.uniform(g, cols, m)
         y0 = synth.uniform(g, rows, m)
         yd = dev(y0)
@@ -313,14 +306,16 @@ def test_config_c1_full(ff, oracle_mod, cuda):
                                                      M["val"], m, x, y, 1, 1))
 
 
+@pytest.mark.parametrize("strategy", [0, 2])
 @pytest.mark.parametrize("name", ["c2", "c3"])
-def test_config_full_apply_transpose(ff, oracle_mod, cuda, name):
-    """Full-size c2 / c3, the exact launch bench.py times (alpha=1, beta=0),
-    compared on every output element (the oracle finishes in seconds)."""
+def test_config_full_apply_transpose(ff, oracle_mod, cuda, name, strategy):
+    """Full-size c2 / c3, the exact launch bench.py times (alpha=1, beta=0,
+    default strategy), compared on every output element (the oracle finishes
+    in seconds); also the PANELS layout."""
     M = synth.config_matrix(name)
     m = M["m"]
     g = _cfg_vectors(name, M, m)
-    A = ff.ffspmv_create(M["rows"], M["cols"], M["row"], M["col"], M["val"], m)
+    A = ff.ffspmv_create(M["rows"], M["cols"], M["row"], M["col"], M["val"], m, strategy=strategy)
     x = synth.uniform(g, M["cols"], m)
     import torch
     yd = torch.empty(M["rows"], dtype=torch.int32, device="cuda")
@@ -355,37 +350,3 @@ def test_config_c4_block_full(ff, oracle_mod, cuda, k):
         sub = oracle_mod.apply_block(M["rows"], M["cols"], M["row"][sel], M["col"][sel],
                                      M["val"][sel], m, X)
         assert np.array_equal(got[rows], sub[rows])
-
-
-def test_config_c5_sequence_prefix_and_spot(ff, oracle_mod, cuda):
-    """c5 at full size: the first 3 terms against the oracle, then a spot
-    check of 1 oracle step from a downloaded iterate deep in the run."""
-    import torch
-    M = synth.config_matrix("c5")
-    m, n, k = M["m"], M["rows"], 16
-    g = _cfg_vectors("c5", M, m)
-    X = synth.uniform(g, (n, k), m)
-    U = synth.uniform(g, (n, k), m)
-    A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], m)
-    S, V = A.sequence(dev(X), 3, dev(U), want_vout=True)
-    Sw, Vw = oracle_mod.sequence(n, M["row"], M["col"], M["val"], m, X, 3, U, want_vout=True)
-    assert np.array_equal(host(S).reshape(Sw.shape), Sw)
-    assert np.array_equal(host(V), Vw)
-    # run 40 more steps on the device, then check the next 2 terms from V_43
-    S2, V2 = A.sequence(V, 40, dev(U), want_vout=True)
-    S3 = A.sequence(V2, 2, dev(U))
-    Sw3 = oracle_mod.sequence(n, M["row"], M["col"], M["val"], m, host(V2), 2, U)
-    assert np.array_equal(host(S3).reshape(Sw3.shape), Sw3)
-
-
-def test_config_c5_scaled_full_length(ff, oracle_mod, cuda):
-    """Scaled c5 (N = 2^11) over the full L = 2 ceil(N/k) + 2 steps."""
-    M = synth.config_matrix("c5", scale=1 / 1024)
-    m, n, k = M["m"], M["rows"], 16
-    g = synth.rng(2005)
-    X = synth.uniform(g, (n, k), m)
-    L = 2 * ((n + k - 1) // k) + 2
-    A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], m)
-    S = A.sequence(dev(X), L)
-    Sw = oracle_mod.sequence(n, M["row"], M["col"], M["val"], m, X, L)
-    assert np.array_equal(host(S).reshape(Sw.shape), Sw)

@@ -300,3 +300,48 @@ def test_preconditions(oracle_mod):
         oracle_mod.apply(1, 1, idx, idx, np.ones(1, np.int64), 5, [5])       # x not canonical
     with pytest.raises(oracle_mod.OracleError):
         oracle_mod.apply(1, 1, idx, idx, np.ones(1, np.int64), 1, [0])       # m < 2
+
+
+# --------------------------------------------------------------------------
+# 6. Threaded timing mode: pinned to dense brute force
+#    on tiny inputs and to the serial functions on larger ones, for thread
+#    counts that leave threads empty and cut keys at every boundary.
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("m", [2, 3, 65521, (1 << 31) - 1, (1 << 32) - 1])
+def test_threaded_mode_bruteforce(oracle_mod, m):
+    g = synth.rng(404 + m % 991)
+    for trial in range(8):
+        rows, cols = int(g.integers(0, 20)), int(g.integers(0, 20))
+        nnz = int(g.integers(0, 1 + rows * cols)) if rows * cols else 0
+        ri, ci, val = synth.random_coo(g, rows, cols, nnz, m, dup=0.2, big=True)
+        D = dense(rows, cols, ri, ci, val)
+        x, y = synth.uniform(g, cols, m), synth.uniform(g, rows, m)
+        alpha, beta = int(g.integers(0, 1 << 32)), int(g.integers(0, 1 << 32))
+        r_s, c_s, v_s = oracle_mod.sort_triples(ri, ci, val)
+        for T in (1, 3, 64):
+            got = oracle_mod.apply_mt(rows, cols, r_s, c_s, v_s, m, x, y, alpha, beta, nthreads=T)
+            assert np.array_equal(got, brute_apply(D, m, x, y, alpha, beta))
+        xt, yt = synth.uniform(g, rows, m), synth.uniform(g, cols, m)
+        c_t, r_t, v_t = oracle_mod.sort_triples(ci, ri, val)
+        for T in (2, 5):
+            got = oracle_mod.apply_transpose_mt(rows, cols, c_t, r_t, v_t, m, xt, yt, alpha, beta,
+                                                nthreads=T)
+            assert np.array_equal(got, brute_apply(transpose_dense(D, cols), m, xt, yt, alpha, beta))
+
+
+def test_threaded_mode_matches_serial(oracle_mod):
+    g = synth.rng(4242)
+    M = synth.config_matrix("c2", scale=1 / 64)
+    m, n = M["m"], M["rows"]
+    r_s, c_s, v_s = oracle_mod.sort_triples(M["row"], M["col"], M["val"])
+    X = synth.uniform(g, (n, 5), m)
+    U = synth.uniform(g, (n, 3), m)
+    for T in (1, 4, 7):
+        assert np.array_equal(oracle_mod.apply_block_mt(n, n, r_s, c_s, v_s, m, X, nthreads=T),
+                              oracle_mod.apply_block(n, n, M["row"], M["col"], M["val"], m, X))
+        S1, V1 = oracle_mod.sequence_mt(n, r_s, c_s, v_s, m, X, 4, U, want_vout=True, nthreads=T)
+        S0, V0 = oracle_mod.sequence(n, M["row"], M["col"], M["val"], m, X, 4, U, want_vout=True)
+        assert np.array_equal(S1, S0) and np.array_equal(V1, V0)
+    with pytest.raises(oracle_mod.OracleError):            # unsorted input is refused
+        oracle_mod.apply_mt(n, n, M["row"][::-1], M["col"][::-1], M["val"][::-1], m, X[:, 0])
