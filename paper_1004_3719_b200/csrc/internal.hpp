@@ -215,13 +215,22 @@ int launch_panel_apply(const DevPanel &op, const DevMod &M, uint32_t alpha, cons
 // Entry word: byte offset of the 32-bit word of the staged panel holding the
 // column's residue in bits [5 + rs, 32), the band row in bits [5, 5 + rs), the
 // residue's bit offset inside that word in bits [0, 5).  Chunk c of a section
-// holds entries [512 c, 512 c + 512) (RUN_E = 16): entry 16 l + j goes to
-// lane l, slot j, at word 512 c + 128 (j / 4) + 4 l + (j % 4) (four coalesced
-// 16-byte loads per lane) and, for values, at 512 c + 16 l + j.  Padding
+// holds entries [256 c, 256 c + 256) (RUN_E = 8): entry 8 l + j goes to lane
+// l, slot j, at word 256 c + 128 (j / 4) + 4 l + (j % 4) (two coalesced
+// 16-byte loads per lane) and, for values, at 256 c + 8 l + j.  Padding
 // entries point at the zero word past the panel (byte offset panel_bytes).
-constexpr uint32_t RUN_E = 16;
+// RUN_E and RUN_WARPS: measured on c3 (tools/time_apply.py, A/B builds of
+// tools/build_variant_flags.sh): 24 warps x 8 entries per lane (72 regs) at
+// 72.7 us beat 32 x 8 (74.8), 16 x 8 (78.9) and 24 x 16 (76.8, spills).
+#ifndef FFSPMV_RUN_E
+#define FFSPMV_RUN_E 8
+#endif
+#ifndef FFSPMV_RUN_WARPS
+#define FFSPMV_RUN_WARPS 24
+#endif
+constexpr uint32_t RUN_E = FFSPMV_RUN_E;
 constexpr uint32_t RUN_CHUNK = 32 * RUN_E;
-constexpr uint32_t RUN_WARPS = 16;    // warps per k_runs CTA, each with private band accumulators
+constexpr uint32_t RUN_WARPS = FFSPMV_RUN_WARPS;   // warps per k_runs CTA, each with private band accumulators
 
 struct RunsGeom {
     uint32_t W = 0, R = 0, P = 0, B = 0;

@@ -14,10 +14,10 @@
 //                (sorted by row), sums each run of one row in a register and
 //                adds it to the warp's accumulators (red.shared) when the row
 //                changes; the unit writes one residue per band row into
-//                partial[p], and the band's last unit to finish (arrival
-//                counter) sums the P partials and writes y (Fig. 2,
-//                P:210-222, "foreach submatrix Ai in A do spmv(y, Ai, x);
-//                reduce(y, m)").
+//                partial[p]
+//   k_runs_reduce  y = alpha sum_p partial[p] + beta y (Fig. 2, P:210-222,
+//                "foreach submatrix Ai in A do spmv(y, Ai, x); reduce(y, m)"),
+//                the programmatic dependent of k_runs
 #include <type_traits>
 
 #include "device.cuh"
@@ -39,13 +39,12 @@ template <int XB>
 __global__ void k_runs_pack(const uint32_t *__restrict__ x, uint32_t cols, uint32_t W, uint32_t P,
                             uint32_t panel_bytes, unsigned char *__restrict__ xp) {
     asm volatile("griddepcontrol.launch_dependents;");
+    // grid: (groups of 256 x 4 elements, panels); 32-bit indices (W < 2^31)
     const uint32_t per_panel = W / 4;
-    const uint64_t total = (uint64_t)P * per_panel;
     const bool aligned = ((uintptr_t)x & 15) == 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t p = i / per_panel, q = i - p * per_panel;
-        const uint64_t c0 = p * W + 4 * q;               // first column
+    for (uint32_t p = blockIdx.y; p < P; p += gridDim.y)
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < per_panel; q += gridDim.x * blockDim.x) {
+        const uint64_t c0 = (uint64_t)p * W + 4 * q;     // first column
         uint4 v;
         if (aligned && c0 + 4 <= cols) {
             v = __ldg(reinterpret_cast<const uint4 *>(x + c0));
@@ -55,7 +54,7 @@ __global__ void k_runs_pack(const uint32_t *__restrict__ x, uint32_t cols, uint3
             v.z = c0 + 2 < cols ? __ldg(x + c0 + 2) : 0u;
             v.w = c0 + 3 < cols ? __ldg(x + c0 + 3) : 0u;
         }
-        unsigned char *dst = xp + p * panel_bytes + q * (XB / 2);   // 4 * XB bits = XB / 2 bytes
+        unsigned char *dst = xp + (uint64_t)p * panel_bytes + (uint64_t)q * (XB / 2);   // 4 * XB bits
         if constexpr (XB == 2) {
             *dst = (unsigned char)(v.x | v.y << 2 | v.z << 4 | v.w << 6);
         } else if constexpr (XB == 4) {
@@ -153,20 +152,26 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint64_t bytes) {
     }
 }
 
-// One lane's share of a chunk: RUN_E = 16 entry words (four coalesced
+// One lane's share of a chunk: RUN_E entry words (RUN_E / 4 coalesced
 // 16-byte loads per warp, 512 contiguous bytes each) and, for a valued chunk,
-// 16 values (lane-contiguous: VB 16-byte loads).
+// RUN_E values (lane-contiguous, RUN_E * VB bytes).
+constexpr int RUN_Q = RUN_E / 4;                      // word quads per lane
 struct ChunkRegs {
-    uint4 w[4], v[4];
+    uint4 w[RUN_Q], v[(RUN_E * 4 + 15) / 16];
 };
 
 template <int VB>
 __device__ __forceinline__ void load_chunk(const uint32_t *wb, const unsigned char *vb, ChunkRegs &c) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) c.w[q] = ld_stream4(wb + 128 * q);
+    for (int q = 0; q < RUN_Q; ++q) c.w[q] = ld_stream4(wb + 128 * q);
     if (vb) {
+        if constexpr (RUN_E * VB >= 16) {
 #pragma unroll
-        for (int q = 0; q < VB; ++q) c.v[q] = ld_stream4(vb + 16 * q);
+            for (int q = 0; q < RUN_E * VB / 16; ++q) c.v[q] = ld_stream4(vb + 16 * q);
+        } else {
+            const uint2 t = ld_stream2(vb);   // RUN_E * VB == 8
+            c.v[0] = make_uint4(t.x, t.y, 0, 0);
+        }
     }
 }
 
@@ -449,10 +454,10 @@ int launch_t(const DevRuns &op, const DevMod &M, uint32_t alpha, const uint32_t 
              uint32_t *y, cudaStream_t st) {
     const RunsGeom &g = op.g;
     // pack x into the panels (4 residues per thread)
-    const uint64_t total = (uint64_t)g.P * (g.W / 4);
-    const uint32_t blocks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 32));
-    k_runs_pack<XB><<<blocks, 256, 0, st>>>(x, op.cols, g.W, g.P, g.panel_bytes,
-                                            reinterpret_cast<unsigned char *>(op.xpack));
+    const uint32_t bx = std::max<uint32_t>(1, std::min<uint32_t>((g.W / 4 + 255) / 256,
+                                                                 (148u * 32 + g.P - 1) / g.P));
+    k_runs_pack<XB><<<dim3(bx, std::min<uint32_t>(g.P, 65535u)), 256, 0, st>>>(x, op.cols, g.W, g.P, g.panel_bytes,
+                                                   reinterpret_cast<unsigned char *>(op.xpack));
     count_launch();
     int e = (int)cudaGetLastError();
     if (e) return e;
@@ -481,6 +486,9 @@ int launch_t(const DevRuns &op, const DevMod &M, uint32_t alpha, const uint32_t 
     count_launch();
     if (e || g.P == 1) return e ? e : (int)cudaGetLastError();
     // y <- the panels' partials, as the programmatic dependent of k_runs
+    // (measured: a fused tail -- arrival counters per band, the CTA
+    // completing a band reduces it -- was slower, 87 vs 73 us on c3: the
+    // bands' last arrivals bunch on a few CTAs)
     const uint32_t nv = (op.rows + 16 / sizeof(PT) - 1) / (16 / sizeof(PT));
     cfg.gridDim = dim3(std::max<uint32_t>(1, std::min<uint32_t>((nv + 255) / 256, g.nctas * 8)));
     cfg.blockDim = dim3(256);

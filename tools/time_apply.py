@@ -26,7 +26,10 @@ def main():
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--transpose", action="store_true")
     ap.add_argument("--opt", nargs="*", default=[])
+    ap.add_argument("--lib", default=None)
     a = ap.parse_args()
+    if a.lib:
+        ff.load(a.lib)
     kw = {k: int(v) for k, v in (o.split("=") for o in a.opt)}
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     M = synth.config_matrix(a.config)
@@ -60,7 +63,7 @@ def main():
                               "alg_gbs": round(alg / ms / 1e6, 1), "frac": round(alg / ms / 1e6 / peak, 4),
                               "panels": info["panels"], "bands": info["panel_bands"],
                               "xbits": info["panel_xbits"], "stream_bytes": info["panel_stream_bytes"],
-                              "opts": kw}), flush=True)
+                              "opts": kw, "lib": a.lib}), flush=True)
         del A
 
 
