@@ -457,8 +457,13 @@ def bench_multi(args, world, rank, local):
 
 
 def _seq_dist(args, world, rank, local):
-    """c5 sequence across the ranks through dist.sequence_2d on the grid
-    grid_shape picks; timed steps bracketed by device events (on_step hook)."""
+    """c5 sequence across the ranks through the C-ABI distributed handle
+    (ffspmv_create with an NCCL communicator; the per-step band SpMM with its
+    fused projection and the ncclAllGather of the band iterates run inside
+    ffspmv_sequence) on the grid grid_shape picks.  Steady-state time per
+    step = (T(L0 + steps) - T(L0)) / steps over two calls, each timed with
+    device events around the call, max over ranks (the difference removes
+    the per-call prologue and the final exchange of S)."""
     import torch
 
     import paper_1004_3719_b200 as ff
@@ -467,32 +472,37 @@ def _seq_dist(args, world, rank, local):
     try:
         M, n, k, X, U = _c5_inputs(synth)
         steps = max(1, args.steps)
-        L = args.warmup + steps + 1          # the last step only projects
-        pr, pc = fdist.grid_shape(world, k, n=n, nnz=len(M["row"]), iterate_bytes=4)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        lc = {}
-
-        def hook(t):
-            if t == args.warmup:
-                torch.cuda.synchronize()
-                torch.distributed.barrier()
-                lc["l0"] = ff.ffspmv_kernel_launches()
-                e0.record()
-            elif t == args.warmup + steps:
-                e1.record()
-                lc["l1"] = ff.ffspmv_kernel_launches()
-                torch.cuda.synchronize()
-
-        fdist.sequence_2d(n, M["row"], M["col"], M["val"], M["m"], X, L, U,
-                          fdist.CudaBackend(f"cuda:{local}"), pr, pc, on_step=hook)
-        ms = e0.elapsed_time(e1)
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
-        return {"steps_per_s": steps / (ms / 1e3), "ms_per_step": ms / steps, "steps": steps,
-                "grid": [pr, pc], "launches": lc["l1"] - lc["l0"],
-                "parallelism": f"2-D grid {pr} x {pc} (row bands x column blocks), "
-                               "NCCL all-gather of the iterate per step"}
+        pr, pc = fdist.grid_shape(world, k, n=n, nnz=len(M["row"]), iterate_bytes=2)
+        comm = ff.comm_from_torch()
+        A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], M["m"], comm=comm, dist_rows=pr)
+        Xd, Ud = to_dev(X), to_dev(U)
+        stream = torch.cuda.current_stream()
+        L0 = max(2, args.warmup)
+        ws = torch.empty(ff.ffspmv_workspace_size(A, ff.OP_SEQUENCE, k, k), dtype=torch.uint8, device="cuda")
+        S = torch.empty((L0 + steps, k, k), dtype=torch.int32, device="cuda")
+        for _ in range(2):                                     # warm-up calls
+            ff.ffspmv_sequence(A, k, Xd, k, Ud, L0, S, None, ws, stream)
+        times, launches = [], 0
+        for L in (L0, L0 + steps):
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0 = ff.ffspmv_kernel_launches()
+            e0.record(stream)
+            ff.ffspmv_sequence(A, k, Xd, k, Ud, L, S, None, ws, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            launches = ff.ffspmv_kernel_launches() - l0
+            tt = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            times.append(float(tt.item()))
+        ms = (times[1] - times[0]) / steps
+        del A
+        comm.close()
+        return {"steps_per_s": 1e3 / ms, "ms_per_step": ms, "steps": steps, "grid": [pr, pc],
+                "launches": launches, "call_ms": times,
+                "parallelism": f"2-D grid {pr} x {pc} (row bands x column blocks), C-ABI "
+                               "distributed handle, ncclAllGather of the u16 band iterates per step"}
     except Exception as e:                       # the line must still print
         return {"error": f"{type(e).__name__}: {e}"[:300]}
 

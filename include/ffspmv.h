@@ -64,6 +64,10 @@ typedef enum {
 /* Opaque matrix handle: A (and by default A^T) packed on one device. */
 typedef struct ffspmv_matrix_s *ffspmv_matrix;
 
+/* Opaque communicator of the distributed sequence (one rank per GPU over
+ * NCCL, or an in-process group for testing): see ffspmv_comm_create. */
+typedef struct ffspmv_comm_s *ffspmv_comm;
+
 /* Band formats (§2.4.4-2.4.5).  AUTO lets the per-band chooser
  * pick the format that moves the fewest HBM bytes. */
 enum {
@@ -119,6 +123,9 @@ typedef struct {
     uint32_t panel_cols;     /* PANELS / RUNS: columns per panel, 0 = default      */
     uint32_t panel_xbits;    /* RUNS: bits per staged x residue, 0 = narrowest for
                                 m; 2, 4, 8, 16, 32 (results must not change)     */
+    ffspmv_comm comm;        /* non-NULL: a DISTRIBUTED handle (see below)        */
+    uint32_t dist_rows;      /* distributed: P_r, the row bands of the P_r x P_c
+                                grid (P_c = ranks / P_r); 0 = all ranks (ROWS)   */
 } ffspmv_options;
 
 /* Summary of a built (or analysed) matrix. */
@@ -155,6 +162,10 @@ typedef struct {
     uint64_t panel_stream_bytes;  /* packed bytes read by one PANELS / RUNS apply  */
     double gather_locality;       /* distinct 128 B x lines / nonzeros (sampled)   */
     uint32_t panel_xbits;         /* bits per staged x residue (PANELS / RUNS)     */
+    uint32_t dist_ranks;          /* distributed handle: ranks (else 0)            */
+    uint32_t dist_grid_rows;      /* P_r of the P_r x P_c grid                     */
+    uint64_t dist_band_row0;      /* first row of this rank's band                 */
+    uint64_t dist_band_rows;      /* rows of this rank's band                      */
 } ffspmv_info;
 
 /* --- lifecycle ------------------------------------------------------------ */
@@ -261,6 +272,43 @@ FFSPMV_API ffspmv_status ffspmv_project(ffspmv_matrix A, uint32_t k, const uint3
  * (e.g. the band projections after an all-gather).  Device pointers. */
 FFSPMV_API ffspmv_status ffspmv_sum_mod(ffspmv_matrix A, uint64_t count, uint32_t nparts,
                                         const uint32_t *parts, uint32_t *out, void *stream);
+
+/* --- distributed sequence ("parallel sequence generation") -------- *
+ *
+ * One rank per GPU.  A communicator comes from NCCL (loaded at run time from
+ * libnccl.so.2, so the library itself has no NCCL link dependency):
+ *   rank 0: ffspmv_comm_unique_id(id); broadcast the 128 bytes (e.g. over a
+ *   torch.distributed process group); every rank: ffspmv_comm_create(&c, id,
+ *   nranks, rank) -- collective, like ncclCommInitRank.
+ * ffspmv_comm_create_local(out[nranks], nranks) makes an in-process group
+ * instead (ranks = host threads on one device, collectives = device copies,
+ * synchronous): the same distributed code path, testable on one GPU.
+ *
+ * A DISTRIBUTED handle: every rank calls ffspmv_create with the FULL triple
+ * list of a square n x n matrix and options.comm (collective).  The ranks
+ * form a P_r x P_c grid (rank = i * P_c + j, P_r = options.dist_rows or all
+ * ranks); rank (i, j) keeps row band i of A (nnz-balanced contiguous bands,
+ * the same on every rank) and, in ffspmv_sequence, column block j of X
+ * (columns [k j / P_c, k (j + 1) / P_c)).  Per step it computes its band of
+ * V_{t+1}[:, block j] (band SpMM + fused band projection) and all-gathers
+ * the band iterates among the P_r ranks of block j on the caller's stream
+ * (NCCL: ncclAllGather over the column-group communicator, an
+ * ncclCommSplit of comm).  P_c = 1 is the row-band mode of P:462-463 ("let
+ * the SpMV library take care of the iteration"), P_r = 1 the column mode of
+ * P:457-460 ("ship independent set of vector blocks ... then gather").
+ * ffspmv_sequence takes the same arguments as on one GPU -- X, U (full
+ * n x k / n x ku, replicated), S (full L x ku x k) and V_out (full) on every
+ * rank -- and returns results identical to the one-GPU call.  Only
+ * ffspmv_sequence, ffspmv_workspace_size and ffspmv_get_info accept a
+ * distributed handle (the others return FFSPMV_ERR_UNSUPPORTED).  Calls on a
+ * distributed handle must not overlap (it owns the result-exchange buffers,
+ * allocated on first use and grown with L). */
+FFSPMV_API ffspmv_status ffspmv_comm_unique_id(void *id_128);
+FFSPMV_API ffspmv_status ffspmv_comm_create(ffspmv_comm *out, const void *id_128, int nranks,
+                                            int rank);
+FFSPMV_API ffspmv_status ffspmv_comm_create_local(ffspmv_comm *out, int nranks);
+/* Destroy after every handle created with it. */
+FFSPMV_API ffspmv_status ffspmv_comm_destroy(ffspmv_comm c);
 
 /* --- diagnostics ------------------------------------------------------------ */
 

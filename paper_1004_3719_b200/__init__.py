@@ -30,6 +30,7 @@ EXPORTS = [
     "ffspmv_apply_transpose", "ffspmv_apply_block", "ffspmv_apply_host",
     "ffspmv_workspace_size", "ffspmv_sequence", "ffspmv_project", "ffspmv_sum_mod",
     "ffspmv_status_string", "ffspmv_last_error", "ffspmv_version", "ffspmv_kernel_launches",
+    "ffspmv_comm_unique_id", "ffspmv_comm_create", "ffspmv_comm_create_local", "ffspmv_comm_destroy",
 ]
 
 
@@ -48,6 +49,8 @@ class ffspmv_options(ctypes.Structure):
         ("panel_rows", ctypes.c_uint32),
         ("panel_cols", ctypes.c_uint32),
         ("panel_xbits", ctypes.c_uint32),
+        ("comm", ctypes.c_void_p),
+        ("dist_rows", ctypes.c_uint32),
     ]
 
 
@@ -89,6 +92,10 @@ class ffspmv_info(ctypes.Structure):
         ("panel_stream_bytes", ctypes.c_uint64),
         ("gather_locality", ctypes.c_double),
         ("panel_xbits", ctypes.c_uint32),
+        ("dist_ranks", ctypes.c_uint32),
+        ("dist_grid_rows", ctypes.c_uint32),
+        ("dist_band_row0", ctypes.c_uint64),
+        ("dist_band_rows", ctypes.c_uint64),
     ]
 
 
@@ -125,6 +132,10 @@ def load(path: str = LIB_PATH):
         "ffspmv_sequence": [P, u32, P, u32, P, u64, P, P, P, ctypes.c_size_t, P],
         "ffspmv_project": [P, u32, P, u32, P, P, P, ctypes.c_size_t, P],
         "ffspmv_sum_mod": [P, u64, u32, P, P, P],
+        "ffspmv_comm_unique_id": [P],
+        "ffspmv_comm_create": [ctypes.POINTER(P), P, i32, i32],
+        "ffspmv_comm_create_local": [P, i32],
+        "ffspmv_comm_destroy": [P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -167,7 +178,8 @@ def _check(rc):
 
 def make_options(device=-1, no_transpose=False, segregate_pm1=0, force_format=FMT_AUTO,
                  band_rows=0, long_row=0, force_acc_bits=0, check_inputs=False,
-                 strategy=STRATEGY_AUTO, panel_rows=0, panel_cols=0, panel_xbits=0):
+                 strategy=STRATEGY_AUTO, panel_rows=0, panel_cols=0, panel_xbits=0, comm=None,
+                 dist_rows=0):
     o = ffspmv_options()
     o.struct_size = ctypes.sizeof(ffspmv_options)
     o.device = device
@@ -182,6 +194,8 @@ def make_options(device=-1, no_transpose=False, segregate_pm1=0, force_format=FM
     o.panel_rows = panel_rows
     o.panel_cols = panel_cols
     o.panel_xbits = panel_xbits
+    o.comm = comm.handle.value if isinstance(comm, Comm) else comm
+    o.dist_rows = dist_rows
     return o
 
 
@@ -381,6 +395,64 @@ def ffspmv_project(A, k, V, ku, U, S, workspace, stream=None):
     _check(load().ffspmv_project(_h(A), k, _ptr(V), ku, _ptr(U), _ptr(S), ws, nbytes,
                                  _stream(stream)))
     return S
+
+
+# ------------------------------------------------------------ communicators ---
+
+class Comm:
+    """A communicator of the distributed sequence (owns the C handle)."""
+
+    def __init__(self, handle: int, nranks: int, rank: int):
+        self.handle = ctypes.c_void_p(handle)
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self.handle.value and _lib is not None:
+            _check(_lib.ffspmv_comm_destroy(self.handle))
+            self.handle = ctypes.c_void_p(0)
+
+
+def ffspmv_comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (call on one rank, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().ffspmv_comm_unique_id(buf))
+    return buf.raw
+
+
+def ffspmv_comm_create(uid: bytes, nranks: int, rank: int) -> Comm:
+    """NCCL communicator (collective over the nranks processes)."""
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(load().ffspmv_comm_create(ctypes.byref(h), buf, nranks, rank))
+    return Comm(h.value, nranks, rank)
+
+
+def ffspmv_comm_create_local(nranks: int):
+    """In-process group of nranks communicators (ranks = host threads on one
+    device) for testing the distributed path on one GPU."""
+    arr = (ctypes.c_void_p * nranks)()
+    _check(load().ffspmv_comm_create_local(arr, nranks))
+    return [Comm(arr[r], nranks, r) for r in range(nranks)]
+
+
+def ffspmv_comm_destroy(c: Comm):
+    c.close()
+
+
+def comm_from_torch(group=None) -> Comm:
+    """NCCL communicator over a torch.distributed process group: rank 0 draws
+    the unique id and broadcasts it over the group (argument marshalling only:
+    the per-step exchange runs inside ffspmv_sequence)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t[:] = torch.frombuffer(bytearray(ffspmv_comm_unique_id()), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return ffspmv_comm_create(bytes(t.cpu().numpy().tobytes()), world, rank)
 
 
 def ffspmv_sum_mod(A, count, nparts, parts, out, stream=None):

@@ -23,8 +23,8 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU_SOURCES = ["seq.cu", "block.cu", "block16.cu", "block16w.cu", "kernels.cu", "panel.cu", "runs.cu"]
-CPP_SOURCES = ["abi.cpp", "builder.cpp", "panel_build.cpp", "runs_build.cpp"]
-HEADERS = ["internal.hpp", "device.cuh", "block.cuh", "seq_mma.cuh"]
+CPP_SOURCES = ["abi.cpp", "builder.cpp", "panel_build.cpp", "runs_build.cpp", "comm.cpp"]
+HEADERS = ["internal.hpp", "device.cuh", "block.cuh", "seq_mma.cuh", "comm.hpp"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -72,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or jobs or _newer(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
         _run([NVCC, "-shared", *GENCODE, "-cudart", "static", "-o", tmp, *objs,
-              "-Xlinker", "--exclude-libs,ALL"])
+              "-Xlinker", "--exclude-libs,ALL", "-ldl"])
         os.replace(tmp, LIB)
     if verbose:
         print("\n".join(logs))

@@ -2,12 +2,15 @@
 // upload, and dispatch to the kernels.  SURVEY §8 row b.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "../../include/ffspmv.h"
+#include "comm.hpp"
 #include "internal.hpp"
 
 using namespace ffspmv;
@@ -52,6 +55,22 @@ bool overlaps(const void *a, size_t an, const void *b, size_t bn) {
 
 }  // namespace
 
+namespace ffspmv {
+ffspmv_status set_error(ffspmv_status s, const std::string &msg) { return fail(s, msg); }
+}  // namespace ffspmv
+
+// State of a distributed handle (rank (i, j) of a P_r x P_c grid).
+struct DistState {
+    CommImpl *world = nullptr;             // the caller's communicator (not owned)
+    CommImpl *group = nullptr;             // ranks of this column block (owned)
+    uint32_t nranks = 1, pr = 1, pc = 1, i = 0, j = 0;
+    uint64_t n = 0;
+    std::vector<uint32_t> bstart;          // P_r + 1 band starts
+    uint32_t rows_max = 1;
+    void *buf = nullptr;                   // result-exchange buffers (grown on demand)
+    size_t buf_bytes = 0;
+};
+
 struct ffspmv_matrix_s {
     int device = 0;
     uint32_t m = 0;
@@ -71,6 +90,7 @@ struct ffspmv_matrix_s {
     size_t stage_elems = 0;
     bool checked = false;              // check_inputs option
     std::mutex mu;
+    DistState *dist = nullptr;         // non-NULL: a distributed handle
 };
 
 namespace {
@@ -218,11 +238,17 @@ ffspmv_status upload_runs(const HostRuns &h, DevRuns &d, DevMem &mem) {
 }
 
 ffspmv_status read_options(const ffspmv_options *o, BuildOptions &bo, int &device, bool &want_t,
-                           bool &checked) {
+                           bool &checked, ffspmv_comm *comm = nullptr, uint32_t *dist_rows = nullptr) {
     device = -1;
     want_t = true;
     checked = false;
+    if (comm) *comm = nullptr;
+    if (dist_rows) *dist_rows = 0;
     if (!o) return FFSPMV_OK;
+    if (o->struct_size >= offsetof(ffspmv_options, dist_rows) + sizeof(o->dist_rows)) {
+        if (comm) *comm = o->comm;
+        if (dist_rows) *dist_rows = o->dist_rows;
+    }
     if (o->struct_size < offsetof(ffspmv_options, strategy))
         return fail(FFSPMV_ERR_INVALID_ARG, "ffspmv_options.struct_size too small");
     device = o->device;
@@ -409,6 +435,21 @@ ffspmv_status build_host(uint64_t rows, uint64_t cols, uint64_t nnz, const uint3
     return FFSPMV_OK;
 }
 
+// nnz-balanced contiguous row bands: b[0] = 0 <= ... <= b[P] = rows, b[r] =
+// the first row with at least r / P of the entries before it (the same
+// partition on every rank: it depends on the matrix only)
+std::vector<uint32_t> row_bands(const Canon &c, uint32_t P) {
+    std::vector<uint32_t> b(P + 1, 0);
+    const uint64_t total = c.ptr.back();
+    for (uint32_t r = 1; r < P; ++r) {
+        const double target = (double)total * r / P;
+        b[r] = (uint32_t)(std::lower_bound(c.ptr.begin(), c.ptr.end(), (uint64_t)std::ceil(target)) - c.ptr.begin());
+        b[r] = std::max(b[r - 1], std::min<uint32_t>(b[r], (uint32_t)c.nrows));
+    }
+    b[P] = (uint32_t)c.nrows;
+    return b;
+}
+
 uint32_t device_sms(int device) {
     int n = 0;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0)
@@ -417,6 +458,103 @@ uint32_t device_sms(int device) {
 }
 
 }  // namespace
+
+ffspmv_status create_dist(ffspmv_matrix *out, uint64_t rows, uint64_t cols, uint64_t nnz,
+                          const uint32_t *row_idx, const uint32_t *col_idx, const int64_t *vals,
+                          uint32_t modulus, BuildOptions bo, int device, bool checked, ffspmv_comm comm,
+                          uint32_t dist_rows, std::chrono::steady_clock::time_point t0) {
+    CommImpl *world = comm_impl(comm);
+    if (!world) return fail(FFSPMV_ERR_INVALID_ARG, "invalid communicator");
+    if (rows != cols) return fail(FFSPMV_ERR_NONSQUARE, "a distributed handle needs a square matrix");
+    const uint32_t nranks = (uint32_t)comm_size(world), rank = (uint32_t)comm_rank(world);
+    const uint32_t pr = dist_rows ? dist_rows : nranks;
+    if (pr < 1 || nranks % pr) return fail(FFSPMV_ERR_INVALID_ARG, "dist_rows must divide the rank count");
+    const uint32_t pc = nranks / pr, bi = rank / pc, bj = rank % pc;
+    int e;
+    if (device < 0 && (e = cudaGetDevice(&device))) return cuda_fail(e, "cudaGetDevice");
+    DeviceGuard guard(device);
+    Canon ca;
+    std::string err;
+    try {
+        if (int rc = canonicalize(ca, rows, cols, nnz, row_idx, col_idx, vals, modulus, err))
+            return fail((ffspmv_status)rc, err);
+    } catch (const std::bad_alloc &) {
+        return fail(FFSPMV_ERR_NOMEM, "host allocation during canonicalisation");
+    }
+    auto *ds = new DistState();
+    ds->world = world;
+    ds->nranks = nranks;
+    ds->pr = pr;
+    ds->pc = pc;
+    ds->i = bi;
+    ds->j = bj;
+    ds->n = rows;
+    ds->bstart = row_bands(ca, pr);
+    uint32_t rmax = 1;
+    for (uint32_t r = 0; r < pr; ++r) rmax = std::max(rmax, ds->bstart[r + 1] - ds->bstart[r]);
+    ds->rows_max = rmax;
+    if ((uint64_t)pr * rmax >= 0x7FFFFFFFull) { delete ds; return fail(FFSPMV_ERR_DIM, "padded iterate too tall"); }
+    // band i, columns renumbered into the padded iterate layout
+    Canon cb;
+    const uint32_t b0 = ds->bstart[bi], b1 = ds->bstart[bi + 1];
+    cb.nrows = b1 - b0;
+    cb.ncols = (uint64_t)pr * rmax;
+    cb.ptr.assign(cb.nrows + 1, 0);
+    try {
+        const uint64_t e0 = ca.ptr[b0], e1 = ca.ptr[b1];
+        cb.idx.resize(e1 - e0);
+        cb.val.assign(ca.val.begin() + e0, ca.val.begin() + e1);
+        for (uint32_t r = 0; r < cb.nrows; ++r) cb.ptr[r + 1] = ca.ptr[b0 + r + 1] - e0;
+        for (uint64_t t = e0; t < e1; ++t) {
+            const uint32_t c = ca.idx[t];
+            const uint32_t q = (uint32_t)(std::upper_bound(ds->bstart.begin(), ds->bstart.end(), c) -
+                                          ds->bstart.begin()) - 1;
+            cb.idx[t - e0] = q * rmax + (c - ds->bstart[q]);
+        }
+        ca = Canon();
+        Built B;
+        pack_operator(B.rows[0], cb, modulus, bo);
+        B.has_rows[0] = true;
+        ffspmv_matrix h = new (std::nothrow) ffspmv_matrix_s();
+        if (!h) { delete ds; return fail(FFSPMV_ERR_NOMEM, "handle allocation"); }
+        h->device = device;
+        h->m = modulus;
+        h->mod = make_mod(modulus);
+        h->dist = ds;
+        ffspmv_status s;
+        if ((s = upload(B.rows[0], h->op[0], h->mem[0]))) { delete ds; delete h; return s; }
+        h->has_op[0] = true;
+        if ((e = cudaMalloc((void **)&h->flag, 256))) {
+            cudaFree(h->mem[0].base);
+            delete ds;
+            delete h;
+            return cuda_fail(e, "cudaMalloc flag");
+        }
+        fill_stats(h->info, B, modulus);
+        h->info.rows = rows;
+        h->info.cols = cols;
+        h->info.nnz_input = nnz;
+        h->info.dist_ranks = nranks;
+        h->info.dist_grid_rows = pr;
+        h->info.dist_band_row0 = b0;
+        h->info.dist_band_rows = b1 - b0;
+        h->info.has_transpose = 0;
+        h->info.device_bytes = h->mem[0].bytes + 256;
+        h->checked = checked;
+        // the column-block communicator: ranks (., j), ordered by band
+        ds->group = comm_split(world, (int)bj, (int)bi, (int)pr, (int)bi, err);
+        if (!ds->group) {
+            ffspmv_destroy(h);
+            return fail(FFSPMV_ERR_NCCL, err);
+        }
+        h->info.create_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = h;
+        return FFSPMV_OK;
+    } catch (const std::bad_alloc &) {
+        delete ds;
+        return fail(FFSPMV_ERR_NOMEM, "host allocation while packing the band");
+    }
+}
 
 extern "C" {
 
@@ -430,7 +568,11 @@ ffspmv_status ffspmv_create(ffspmv_matrix *out, uint64_t rows, uint64_t cols, ui
     BuildOptions bo;
     int device;
     bool want_t, checked;
-    if ((s = read_options(opts, bo, device, want_t, checked))) return s;
+    ffspmv_comm comm = nullptr;
+    uint32_t dist_rows = 0;
+    if ((s = read_options(opts, bo, device, want_t, checked, &comm, &dist_rows))) return s;
+    if (comm) return create_dist(out, rows, cols, nnz, row_idx, col_idx, vals, modulus, bo, device, checked,
+                                 comm, dist_rows, t0);
     if (device < 0) {
         int e = cudaGetDevice(&device);
         if (e) return cuda_fail(e, "cudaGetDevice");
@@ -499,6 +641,11 @@ ffspmv_status ffspmv_destroy(ffspmv_matrix A) {
         if (mem.base) cudaFree(mem.base);
     if (A->flag) cudaFree(A->flag);
     if (A->stage) cudaFree(A->stage);
+    if (A->dist) {
+        if (A->dist->buf) cudaFree(A->dist->buf);
+        comm_free(A->dist->group);
+        delete A->dist;
+    }
     delete A;
     return FFSPMV_OK;
 }
@@ -570,9 +717,14 @@ ffspmv_status check_vec(ffspmv_matrix A, const uint32_t *v, uint64_t n, uint64_t
     return FFSPMV_OK;
 }
 
+ffspmv_status no_dist(ffspmv_matrix A) {
+    return fail(FFSPMV_ERR_UNSUPPORTED, "a distributed handle supports ffspmv_sequence only");
+}
+
 ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_t *x, uint64_t nx,
                        uint32_t beta, uint32_t *y, uint64_t ny, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (A->dist) return no_dist(A);
     if (!A->has_op[which] && !A->has_pan[which] && !A->has_run[which])
         return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built (no_transpose was set)");
     uint64_t orows, ocols;
@@ -595,6 +747,87 @@ ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_
     return FFSPMV_OK;
 }
 
+// in-place all-gather of the band iterates among the ranks of a column block
+int dist_exchange(void *ctx, void *buf, size_t bytes, void *stream) {
+    DistState *d = (DistState *)ctx;
+    std::string err;
+    const int e = comm_allgather(d->group, (char *)buf + (size_t)d->i * bytes, buf, bytes, stream, err);
+    if (e) fail(e < 0 ? FFSPMV_ERR_NCCL : FFSPMV_ERR_CUDA, err);
+    return e;
+}
+
+ffspmv_status dist_status(int e, const char *where) {
+    if (e < 0) return FFSPMV_ERR_NCCL;          // message already recorded
+    return cuda_fail(e, where);
+}
+
+ffspmv_status sequence_dist(ffspmv_matrix A, uint32_t k, const uint32_t *X, uint32_t ku, const uint32_t *U,
+                            uint64_t L, uint32_t *S, uint32_t *V_out, void *workspace, size_t workspace_bytes,
+                            void *stream) {
+    DistState &d = *A->dist;
+    const DevOp &op = A->op[0];
+    const uint32_t c0 = (uint32_t)((uint64_t)k * d.j / d.pc);
+    const uint32_t kc = (uint32_t)((uint64_t)k * (d.j + 1) / d.pc) - c0;
+    const uint32_t kcmax = (k + d.pc - 1) / d.pc;
+    const size_t need = sequence_dist_workspace(op, A->mod, std::max<uint32_t>(kc, 1), ku, d.pr);
+    if (!workspace || workspace_bytes < need)
+        return fail(FFSPMV_ERR_NOMEM, "workspace smaller than ffspmv_workspace_size (" + std::to_string(need) +
+                                          " bytes)");
+    ffspmv_status s;
+    if ((s = check_vec(A, X, d.n, k, k, stream, "X"))) return s;
+    if (U && (s = check_vec(A, U, d.n, ku, ku, stream, "U"))) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    int e;
+    if (L == 0) {
+        if (V_out && d.n && (e = cudaMemcpyAsync(V_out, X, d.n * k * 4ull, cudaMemcpyDeviceToDevice, st)))
+            return cuda_fail(e, "copy V_out");
+        return FFSPMV_OK;
+    }
+    // exchange buffers: band residues T (one slot), all slots G, band V_L
+    // block Vb and all blocks Gv, the band starts on the device
+    const size_t tslot = (size_t)L * ku * kcmax * 4, vslot = (size_t)d.rows_max * kcmax * 4;
+    const size_t want = tslot * (1 + d.nranks) + (V_out ? vslot * (1 + d.nranks) : 0) + 4 * (d.pr + 1) + 4096;
+    if (want > d.buf_bytes) {
+        if (d.buf) cudaFree(d.buf);
+        d.buf = nullptr;
+        d.buf_bytes = 0;
+        if ((e = cudaMalloc(&d.buf, want))) return cuda_fail(e, "cudaMalloc exchange buffers");
+        d.buf_bytes = want;
+    }
+    char *p = (char *)d.buf;
+    uint32_t *T = (uint32_t *)p;
+    uint32_t *G = (uint32_t *)(p + a256(tslot));
+    uint32_t *bdev = (uint32_t *)(p + a256(tslot) + a256(tslot * d.nranks));
+    uint32_t *Vb = (uint32_t *)((char *)bdev + a256(4 * (d.pr + 1)));
+    uint32_t *Gv = (uint32_t *)((char *)Vb + a256(vslot));
+    if (kc) {
+        DistSeq ds;
+        ds.pr = d.pr;
+        ds.rows_max = d.rows_max;
+        ds.bstart = d.bstart.data();
+        ds.row0 = d.bstart[d.i];
+        ds.own = (uint64_t)d.i * d.rows_max;
+        ds.c0 = c0;
+        ds.kc = kc;
+        ds.exchange = dist_exchange;
+        ds.ctx = &d;
+        e = launch_sequence_dist(op, A->mod, X, k, ku, U, L, T, V_out ? Vb : nullptr, workspace, ds, stream);
+        if (e) return dist_status(e, "distributed sequence");
+    }
+    std::string err;
+    if ((e = comm_allgather(d.world, T, G, tslot, stream, err))) return fail(e < 0 ? FFSPMV_ERR_NCCL : FFSPMV_ERR_CUDA, err);
+    if ((e = launch_dist_sum_S(G, L, ku, k, kcmax, d.pr, d.pc, A->mod, S, stream))) return cuda_fail(e, "sum S");
+    if (V_out) {
+        if ((e = cudaMemcpyAsync(bdev, d.bstart.data(), 4ull * (d.pr + 1), cudaMemcpyHostToDevice, st)))
+            return cuda_fail(e, "band starts");
+        if ((e = comm_allgather(d.world, Vb, Gv, vslot, stream, err)))
+            return fail(e < 0 ? FFSPMV_ERR_NCCL : FFSPMV_ERR_CUDA, err);
+        if ((e = launch_dist_put_V(Gv, d.n, k, kcmax, d.rows_max, d.pr, d.pc, bdev, V_out, stream)))
+            return cuda_fail(e, "assemble V_out");
+    }
+    return FFSPMV_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -614,6 +847,7 @@ ffspmv_status ffspmv_apply_block(ffspmv_matrix A, uint32_t k, uint32_t alpha, co
                                  uint64_t ldx, uint32_t beta, uint32_t *Y, uint64_t ldy,
                                  void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (A->dist) return no_dist(A);
     if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
     if (ldx < k || ldy < k) return fail(FFSPMV_ERR_INVALID_ARG, "leading dimension < k");
     const DevOp &op = A->op[0];
@@ -636,6 +870,7 @@ ffspmv_status ffspmv_apply_block(ffspmv_matrix A, uint32_t k, uint32_t alpha, co
 ffspmv_status ffspmv_apply_host(ffspmv_matrix A, int which, uint32_t alpha, const uint32_t *x_host,
                                 uint32_t beta, uint32_t *y_host, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (A->dist) return no_dist(A);
     if (which != FFSPMV_OP_APPLY && which != FFSPMV_OP_TRANSPOSE)
         return fail(FFSPMV_ERR_INVALID_ARG, "op must be FFSPMV_OP_APPLY or FFSPMV_OP_TRANSPOSE");
     if (!A->has_op[which] && !A->has_pan[which] && !A->has_run[which])
@@ -684,6 +919,12 @@ ffspmv_status ffspmv_workspace_size(ffspmv_matrix A, int which, uint32_t k, uint
     if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
     if (ku == 0) ku = k;
     DeviceGuard guard(A->device);
+    if (A->dist) {
+        const DistState &d = *A->dist;
+        const uint32_t kc = (uint32_t)((uint64_t)k * (d.j + 1) / d.pc - (uint64_t)k * d.j / d.pc);
+        *bytes = sequence_dist_workspace(A->op[0], A->mod, std::max<uint32_t>(kc, 1), ku, d.pr);
+        return FFSPMV_OK;
+    }
     *bytes = sequence_workspace(A->op[0], A->mod, k, ku);
     return FFSPMV_OK;
 }
@@ -693,7 +934,7 @@ ffspmv_status ffspmv_sequence(ffspmv_matrix A, uint32_t k, const uint32_t *X, ui
                               void *workspace, size_t workspace_bytes, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
     const DevOp &op = A->op[0];
-    if (op.rows != op.cols) return fail(FFSPMV_ERR_NONSQUARE, "sequence needs a square matrix");
+    if (!A->dist && op.rows != op.cols) return fail(FFSPMV_ERR_NONSQUARE, "sequence needs a square matrix");
     if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
     if (!U) {
         if (ku != 0 && ku != k) return fail(FFSPMV_ERR_INVALID_ARG, "U == NULL requires ku == k");
@@ -701,7 +942,7 @@ ffspmv_status ffspmv_sequence(ffspmv_matrix A, uint32_t k, const uint32_t *X, ui
     } else if (ku == 0) {
         return fail(FFSPMV_ERR_INVALID_ARG, "ku must be >= 1");
     }
-    const uint64_t n = op.rows;
+    const uint64_t n = A->dist ? A->dist->n : op.rows;
     // the step kernels index the iterate with 32-bit element offsets
     if (n * k >= (1ull << 32) || n * ku >= (1ull << 32))
         return fail(FFSPMV_ERR_DIM, "n * k and n * ku must be < 2^32 elements");
@@ -713,6 +954,7 @@ ffspmv_status ffspmv_sequence(ffspmv_matrix A, uint32_t k, const uint32_t *X, ui
         overlaps(S, L * ku * k * 4ull, U, n * ku * 4ull))
         return fail(FFSPMV_ERR_INVALID_ARG, "S / V_out overlap an input");
     DeviceGuard guard(A->device);
+    if (A->dist) return sequence_dist(A, k, X, ku, U, L, S, V_out, workspace, workspace_bytes, stream);
     size_t need = sequence_workspace(op, A->mod, k, ku);
     if (n && (!workspace || workspace_bytes < need))
         return fail(FFSPMV_ERR_NOMEM, "workspace smaller than ffspmv_workspace_size (" +
@@ -736,6 +978,7 @@ ffspmv_status ffspmv_project(ffspmv_matrix A, uint32_t k, const uint32_t *V, uin
                              const uint32_t *U, uint32_t *S, void *workspace,
                              size_t workspace_bytes, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
+    if (A->dist) return no_dist(A);
     if (k == 0 || ku == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k and ku must be >= 1");
     const uint64_t n = A->op[0].rows;
     if ((n && (!V || !U)) || !S) return fail(FFSPMV_ERR_INVALID_ARG, "NULL V, U or S");

@@ -317,6 +317,27 @@ int launch_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t
                     void *ws, size_t ws_bytes, void *stream);
 int launch_check_canonical(const uint32_t *v, uint64_t n, uint64_t ld, uint64_t w, uint32_t m,
                            uint32_t *flag_dev, void *stream);
+
+// distributed sequence (seq.cu): rank (i, j) of a P_r x P_c grid
+struct DistSeq {
+    uint32_t pr, rows_max;         // row bands, rows of a padded band slot
+    const uint32_t *bstart;        // HOST: P_r + 1 band starts
+    uint64_t row0;                 // first row of this rank's band
+    uint64_t own;                  // this rank's slot: i * rows_max
+    uint32_t c0, kc;               // this rank's column block of X
+    // in-place all-gather of buf (P_r slots of bytes_per_rank) among the P_r
+    // ranks of this column block, on stream (0 or a cudaError_t / -1 for NCCL)
+    int (*exchange)(void *ctx, void *buf, size_t bytes_per_rank, void *stream);
+    void *ctx;
+};
+size_t sequence_dist_workspace(const DevOp &op, const DevMod &M, uint32_t kc, uint32_t ku, uint32_t pr);
+int launch_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint32_t k, uint32_t ku,
+                         const uint32_t *U, uint64_t L, uint32_t *S_band, uint32_t *V_band, void *ws,
+                         const DistSeq &d, void *stream);
+int launch_dist_sum_S(const uint32_t *G, uint64_t L, uint32_t ku, uint32_t k, uint32_t kcmax, uint32_t pr,
+                      uint32_t pc, const DevMod &M, uint32_t *S, void *stream);
+int launch_dist_put_V(const uint32_t *Gv, uint64_t n, uint32_t k, uint32_t kcmax, uint32_t rows_max,
+                      uint32_t pr, uint32_t pc, const uint32_t *bstart_dev, uint32_t *V_out, void *stream);
 uint64_t kernel_launch_count();
 
 }  // namespace ffspmv

@@ -638,4 +638,281 @@ int launch_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t
     return run_sequence<uint32_t>(op, M, k, X, ku, U, L, S, V_out, ws, st);
 }
 
+// ------------------------------------------------- distributed sequence ----
+// Rank (i, j) of a P_r x P_c grid: band i of A (its
+// columns renumbered into the padded iterate layout, q = band(c) * rows_max
+// + c - b_band) and column block j of X.  The iterate V_t[:, block j] lives
+// in the padded layout (P_r * rows_max rows); a step computes the band's rows
+// of V_{t+1} straight into the rank's own slot of the next buffer and the
+// exchange callback all-gathers the slots among the P_r ranks of block j.
+// S_band[t] receives the band's projection residues U_band^T V_t[band, j].
+namespace {
+
+template <class IT>
+__global__ void k_dist_prep(const uint32_t *__restrict__ X, uint32_t k, uint32_t c0, uint32_t kc,
+                            uint64_t npad, uint32_t rows_max, const uint32_t *__restrict__ bstart,
+                            IT *__restrict__ V0) {
+    const uint64_t total = npad * kc;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = e / kc;
+        const uint32_t c = (uint32_t)(e - q * kc);
+        const uint32_t band = (uint32_t)(q / rows_max), r = (uint32_t)(q - (uint64_t)band * rows_max);
+        const uint32_t b0 = bstart[band], h = bstart[band + 1] - b0;
+        V0[e] = r < h ? (IT)X[(uint64_t)(b0 + r) * k + c0 + c] : (IT)0;
+    }
+}
+
+// band copies: Xb = X[row0 .. row0 + h, c0 .. c0 + kc), Ub = U[row0 .. row0 + h, :]
+__global__ void k_dist_band(const uint32_t *__restrict__ X, uint32_t k, uint32_t c0, uint32_t kc,
+                            const uint32_t *__restrict__ U, uint32_t ku, uint64_t row0, uint64_t h,
+                            uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ub) {
+    const uint64_t nx = h * kc, total = nx + h * ku;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        if (e < nx) {
+            const uint64_t r = e / kc;
+            Xb[e] = X[(row0 + r) * k + c0 + (e - r * kc)];
+        } else {
+            const uint64_t f = e - nx;
+            Ub[f] = U[row0 * ku + f];
+        }
+    }
+}
+
+template <class IT, int KUP>
+__global__ void k_dist_upad(const uint32_t *__restrict__ Ub, uint64_t h, uint32_t ku, IT *__restrict__ Uc) {
+    const uint64_t total = h * KUP;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = e / KUP;
+        const uint32_t a = (uint32_t)(e - r * KUP);
+        Uc[e] = a < ku ? (IT)Ub[r * ku + a] : (IT)0;
+    }
+}
+
+template <class IT>
+struct DistLayout {
+    IT *V[2];
+    uint32_t *Xb, *Ub;
+    IT *Uc;
+    uint32_t *partial[2];
+    uint32_t *ufrag;
+    DevOp *opdev;
+    uint32_t *bstart;
+    size_t bytes;
+};
+
+template <class IT>
+DistLayout<IT> dist_layout(void *ws, const DevOp &op, uint32_t m, uint32_t kc, uint32_t ku, uint32_t pr) {
+    DistLayout<IT> L{};
+    const uint64_t h = op.rows, npad = op.cols;
+    char *p = (char *)ws;
+    size_t off = 0;
+    const bool mma = sizeof(IT) == 2 && mma_ok(m, kc, ku);
+    const bool fused = mma || fused_ok(kc, ku);
+    const uint32_t ucols = mma ? 0 : fused_ok(kc, ku) ? kup_for(ku) : ku;
+    const uint32_t nctas = proj_ctas(h);
+    const uint32_t maxc = fused ? std::max<uint32_t>(nctas, (uint32_t)num_sms() * MAX_STEP_CTAS_PER_SM) : nctas;
+    auto take = [&](size_t b) { void *q = p + off; off += align256(b); return q; };
+    L.V[0] = (IT *)take(npad * (size_t)kc * sizeof(IT));
+    L.V[1] = (IT *)take(npad * (size_t)kc * sizeof(IT));
+    L.Xb = (uint32_t *)take(h * (size_t)kc * 4);
+    L.Ub = (uint32_t *)take(h * (size_t)ku * 4);
+    L.Uc = (IT *)take(h * (size_t)ucols * sizeof(IT));
+    L.partial[0] = (uint32_t *)take((size_t)maxc * ku * kc * 4);
+    L.partial[1] = (uint32_t *)take(fused ? (size_t)maxc * ku * kc * 4 : 0);
+    L.ufrag = (uint32_t *)take(mma ? (size_t)op.n_slices * 256 * 4 : 0);
+    L.opdev = (DevOp *)take(sizeof(DevOp));
+    L.bstart = (uint32_t *)take((size_t)(pr + 1) * 4);
+    L.bytes = off;
+    return L;
+}
+
+template <class IT>
+int run_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint32_t k, uint32_t ku,
+                      const uint32_t *U, uint64_t L, uint32_t *S_band, uint32_t *V_band, void *ws,
+                      const DistSeq &d, cudaStream_t st) {
+    const uint64_t h = op.rows, npad = op.cols;
+    const uint32_t kc = d.kc, pairs = ku * kc;
+    DistLayout<IT> W = dist_layout<IT>(ws, op, M.m, kc, ku, d.pr);
+    const uint32_t *Uu = U ? U : X;
+    const uint32_t grid = (uint32_t)num_sms() * 8;
+    int err;
+    if ((err = (int)cudaMemcpyAsync(W.opdev, &op, sizeof(DevOp), cudaMemcpyHostToDevice, st))) return err;
+    if ((err = (int)cudaMemcpyAsync(W.bstart, d.bstart, (d.pr + 1) * 4ull, cudaMemcpyHostToDevice, st))) return err;
+    k_dist_prep<IT><<<grid, 256, 0, st>>>(X, k, d.c0, kc, npad, d.rows_max, W.bstart, W.V[0]);
+    count_launch();
+    if (h) {
+        k_dist_band<<<grid, 256, 0, st>>>(X, k, d.c0, kc, Uu, ku, d.row0, h, W.Xb, W.Ub);
+        count_launch();
+    }
+    const bool mma = sizeof(IT) == 2 && mma_ok(M.m, kc, ku);
+    const bool fused = mma || fused_ok(kc, ku);
+    const uint32_t ldu = mma ? ku : fused ? kup_for(ku) : ku;
+    if (h && mma && op.n_slices) {
+        const uint64_t words = (uint64_t)op.n_slices * 256;
+        k_seq_ufrag<<<(uint32_t)std::min<uint64_t>((words + 255) / 256, grid), 256, 0, st>>>(
+            W.Ub, ku, op.perm, op.slices, op.n_slices, W.ufrag);
+        count_launch();
+    }
+    if (h && !mma && fused) {
+        if (ldu == 16) k_dist_upad<IT, 16><<<grid, 256, 0, st>>>(W.Ub, h, ku, W.Uc);
+        else k_dist_upad<IT, 32><<<grid, 256, 0, st>>>(W.Ub, h, ku, W.Uc);
+        count_launch();
+    }
+    const IT *Ufused = mma ? nullptr : fused ? W.Uc : nullptr;
+    const uint32_t nctas = proj_ctas(std::max<uint64_t>(h, 1));
+    auto project_band = [&](const uint32_t *V32, const IT *Vn, uint32_t *S_t) -> int {
+        if (!h) return (int)cudaMemsetAsync(S_t, 0, (size_t)pairs * 4, st);
+        if (V32) return project<uint32_t>(V32, W.Ub, ku, M, h, kc, ku, W.partial[0], nctas, S_t, st);
+        return project<IT>(Vn, W.Uc, ldu, M, h, kc, ku, W.partial[0], nctas, S_t, st);
+    };
+    const size_t slot = (size_t)d.rows_max * kc;   // elements of one rank's slot
+    if (!fused) {
+        // unfused: project the band, then the band's block apply into its slot
+        if (!mma && ldu == ku && h) {
+            k_seq_prep<IT><<<grid, 256, 0, st>>>(Uu + d.row0 * ku, nullptr, h * (uint64_t)ku, 0, W.Uc, nullptr);
+            count_launch();
+        }
+        for (uint64_t t = 0; t < L; ++t) {
+            const IT *Vt = W.V[t & 1];
+            if ((err = t == 0 ? project_band(W.Xb, nullptr, S_band) :
+                                project_band(nullptr, Vt + d.own * kc, S_band + t * pairs)))
+                return err;
+            if (t + 1 < L) {
+                if (h && (err = launch_block_t<IT, IT>(op, M, kc, 1u, Vt, kc, 0u, W.V[(t + 1) & 1] + d.own * kc,
+                                                      kc, (void *)st)))
+                    return err;
+                if ((err = d.exchange(d.ctx, W.V[(t + 1) & 1], slot * sizeof(IT), (void *)st))) return err;
+            }
+        }
+    } else {
+        if (h) {
+            if ((err = project<uint32_t>(W.Xb, W.Ub, ku, M, h, kc, ku, W.partial[0], nctas, nullptr, st)))
+                return err;                                              // S_0 partials
+        } else if ((err = (int)cudaMemsetAsync(S_band, 0, (size_t)L * pairs * 4, st))) {
+            return err;
+        }
+        uint32_t nprev = nctas;
+        for (uint64_t t = 1; t < L; ++t) {
+            uint32_t nc = nprev;
+            const IT *Vin = W.V[(t - 1) & 1];
+            IT *Vout = W.V[t & 1] + d.own * kc;
+            if (h) {
+                uint32_t *po = W.partial[t & 1];
+                const uint32_t *pp = W.partial[(t - 1) & 1];
+                uint32_t *Sp = S_band + (t - 1) * pairs;
+                if constexpr (sizeof(IT) == 2) {
+                    if (mma) {
+                        err = M.vbytes == 1
+                                  ? launch_step_mma<uint8_t>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp, nprev, Sp, nc, st)
+                                  : launch_step_mma<uint16_t>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp, nprev, Sp, nc, st);
+                    } else {
+                        err = launch_step<IT>(op, M, kc, ku, Vin, Vout, Ufused, po, pp, nprev, Sp, nc, st);
+                    }
+                } else {
+                    err = launch_step<IT>(op, M, kc, ku, Vin, Vout, Ufused, po, pp, nprev, Sp, nc, st);
+                }
+                if (err) return err;
+            }
+            nprev = nc;
+            if ((err = d.exchange(d.ctx, W.V[t & 1], slot * sizeof(IT), (void *)st))) return err;
+        }
+        if (h && L) {
+            k_seq_finalize<<<(pairs + 7) / 8, 256, 0, st>>>(W.partial[(L - 1) & 1], nprev, pairs, M,
+                                                           S_band + (L - 1) * pairs);
+            count_launch();
+        }
+    }
+    if (V_band && h && L) {
+        if ((err = launch_block_t<IT, uint32_t>(op, M, kc, 1u, W.V[(L - 1) & 1], kc, 0u, V_band, kc, (void *)st)))
+            return err;
+    }
+    return (int)cudaGetLastError();
+}
+
+// S[t][a][c_j + c] = sum_i G_(i, j)[t][a][c] mod m over the P_r row bands;
+// G = the all-gathered band residues, rank (i, j)'s slot at (i P_c + j)
+// L ku kcmax holding L x ku x kc_j (c_j = k j / P_c, kc_j = c_{j+1} - c_j)
+__device__ __forceinline__ uint32_t col_block(uint32_t col, uint32_t k, uint32_t pc) {
+    uint32_t j = (uint32_t)(((uint64_t)col * pc) / k);
+    while (j > 0 && (uint64_t)k * j / pc > col) --j;
+    while (j + 1 < pc && (uint64_t)k * (j + 1) / pc <= col) ++j;
+    return j;
+}
+
+__global__ void k_dist_sum_S(const uint32_t *__restrict__ G, uint64_t L, uint32_t ku, uint32_t k,
+                             uint32_t kcmax, uint32_t pr, uint32_t pc, DevMod M, uint32_t *__restrict__ S) {
+    const uint64_t total = L * ku * (uint64_t)k;
+    const uint64_t slot = L * ku * (uint64_t)kcmax;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t ta = e / k;
+        const uint32_t col = (uint32_t)(e - ta * k);
+        const uint32_t j = col_block(col, k, pc);
+        const uint32_t cj = (uint32_t)((uint64_t)k * j / pc), kcj = (uint32_t)((uint64_t)k * (j + 1) / pc) - cj;
+        uint64_t s = 0;   // P_r residues: exact
+        for (uint32_t i = 0; i < pr; ++i) s += G[(uint64_t)(i * pc + j) * slot + ta * kcj + (col - cj)];
+        S[e] = mod64(s, M);
+    }
+}
+
+// V_out[b_i + r][c_j + c] = Gv_(i, j)[r][c] (the all-gathered band blocks of
+// V_L, rank (i, j)'s slot at (i P_c + j) rows_max kcmax holding h_i x kc_j)
+__global__ void k_dist_put_V(const uint32_t *__restrict__ Gv, uint64_t n, uint32_t k, uint32_t kcmax,
+                             uint32_t rows_max, uint32_t pr, uint32_t pc, const uint32_t *__restrict__ bstart,
+                             uint32_t *__restrict__ V_out) {
+    const uint64_t total = n * k;
+    const uint64_t slot = (uint64_t)rows_max * kcmax;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t row = e / k;
+        const uint32_t col = (uint32_t)(e - row * k);
+        uint32_t lo = 0, hi = pr;   // band: the last i with bstart[i] <= row
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (bstart[mid] <= row) lo = mid; else hi = mid;
+        }
+        const uint32_t j = col_block(col, k, pc);
+        const uint32_t cj = (uint32_t)((uint64_t)k * j / pc), kcj = (uint32_t)((uint64_t)k * (j + 1) / pc) - cj;
+        V_out[e] = Gv[(uint64_t)(lo * pc + j) * slot + (row - bstart[lo]) * kcj + (col - cj)];
+    }
+}
+
+}  // namespace
+
+size_t sequence_dist_workspace(const DevOp &op, const DevMod &M, uint32_t kc, uint32_t ku, uint32_t pr) {
+    if (M.m <= 65536u) return dist_layout<uint16_t>(nullptr, op, M.m, kc, ku, pr).bytes;
+    return dist_layout<uint32_t>(nullptr, op, M.m, kc, ku, pr).bytes;
+}
+
+int launch_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint32_t k, uint32_t ku,
+                         const uint32_t *U, uint64_t L, uint32_t *S_band, uint32_t *V_band, void *ws,
+                         const DistSeq &d, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (M.m <= 65536u) return run_sequence_dist<uint16_t>(op, M, X, k, ku, U, L, S_band, V_band, ws, d, st);
+    return run_sequence_dist<uint32_t>(op, M, X, k, ku, U, L, S_band, V_band, ws, d, st);
+}
+
+int launch_dist_sum_S(const uint32_t *G, uint64_t L, uint32_t ku, uint32_t k, uint32_t kcmax, uint32_t pr,
+                      uint32_t pc, const DevMod &M, uint32_t *S, void *stream) {
+    const uint64_t total = L * ku * (uint64_t)k;
+    if (!total) return 0;
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((total + 255) / 256, (uint64_t)num_sms() * 8);
+    k_dist_sum_S<<<blocks, 256, 0, (cudaStream_t)stream>>>(G, L, ku, k, kcmax, pr, pc, M, S);
+    count_launch();
+    return (int)cudaGetLastError();
+}
+
+int launch_dist_put_V(const uint32_t *Gv, uint64_t n, uint32_t k, uint32_t kcmax, uint32_t rows_max,
+                      uint32_t pr, uint32_t pc, const uint32_t *bstart_dev, uint32_t *V_out, void *stream) {
+    const uint64_t total = n * k;
+    if (!total) return 0;
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((total + 255) / 256, (uint64_t)num_sms() * 8);
+    k_dist_put_V<<<blocks, 256, 0, (cudaStream_t)stream>>>(Gv, n, k, kcmax, rows_max, pr, pc, bstart_dev, V_out);
+    count_launch();
+    return (int)cudaGetLastError();
+}
+
 }  // namespace ffspmv

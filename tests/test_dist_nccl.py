@@ -1,8 +1,10 @@
-"""The multi-GPU drivers (dist.py) on the CUDA backend over NCCL, launched as
-one rank on the one GPU a test box has (grid 1 x 1): the same code path the
-bench's N > 1 sequence line takes (CudaBackend, NCCL process groups and
-all-gathers, the on_step timing hook), checked bit-exactly against the oracle
-(P:457-463).  The N > 1 partition logic itself is covered by the gloo tests."""
+"""The multi-GPU paths over NCCL, launched as one rank on the one GPU a test
+box has (grid 1 x 1), checked bit-exactly against the oracle:
+the Python drivers of dist.py (CudaBackend, NCCL process groups and
+all-gathers, the on_step timing hook) and the C-ABI distributed handle over
+a real NCCL communicator (ffspmv_comm_create from a unique id broadcast over
+the torch group).  The N > 1 partition logic is covered by the gloo tests
+and, through the C ABI, by tests/test_gpu_dist.py (in-process ranks)."""
 import os
 import subprocess
 import sys
@@ -32,6 +34,19 @@ assert np.array_equal(S, So) and np.array_equal(V, Vo), "sequence_2d != oracle"
 assert seen == list(range(L + 1)), seen
 Sr = fdist.sequence_rows(n, M["row"], M["col"], M["val"], m, X, L, U, fdist.CudaBackend("cuda:0"))
 assert np.array_equal(Sr, So), "sequence_rows != oracle"
+# the C-ABI distributed handle over a real NCCL communicator (1 x 1 grid):
+# unique id broadcast over the torch group, ncclCommInitRank, ncclCommSplit,
+# the per-step ncclAllGather and the result exchanges
+import paper_1004_3719_b200 as ff
+c = ff.comm_from_torch()
+A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], m, comm=c)
+Xd = torch.from_numpy(X.view(np.int32)).cuda(); Ud = torch.from_numpy(U.view(np.int32)).cuda()
+S2, V2 = A.sequence(Xd, L, Ud, want_vout=True)
+torch.cuda.synchronize()
+assert np.array_equal(S2.cpu().numpy().view(np.uint32).reshape(So.shape), So), "C-ABI dist S != oracle"
+assert np.array_equal(V2.cpu().numpy().view(np.uint32), Vo), "C-ABI dist V != oracle"
+del A
+c.close()
 dist.destroy_process_group()
 print("nccl dist ok")
 '''
