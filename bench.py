@@ -378,23 +378,26 @@ def extras(ff, flush, stream, hbm_peak, args):
     res["c5_sequence"] = _seq_single(ff, stream, hbm_peak, args)
     # c5 oracle seconds per step (threaded mode, 2 steps, extrapolated to L)
     res["c5_sequence"]["cpu_baseline"] = _c5_oracle(oracle, synth)
+    # the GL7d-shaped matrix (square variant) mod 3: the sequence with a u8
+    # iterate (SURVEY a-8)
+    res["c3sq_sequence_m3"] = _seq_single(ff, stream, hbm_peak, args, cfg="c3sq")
     return res
 
 
-def _c5_inputs(synth):
-    M = synth.config_matrix("c5")
+def _c5_inputs(synth, cfg="c5"):
+    M = synth.config_matrix("c5") if cfg == "c5" else synth.config_matrix("c3", square=True)
     n, k = M["rows"], 16
-    g = synth.rng(2005)
+    g = synth.rng(2005 if cfg == "c5" else 2033)
     X = synth.uniform(g, (n, k), M["m"])
     U = synth.uniform(g, (n, k), M["m"])
     return M, n, k, X, U
 
 
-def _seq_single(ff, stream, hbm_peak, args):
+def _seq_single(ff, stream, hbm_peak, args, cfg="c5"):
     import torch
 
     import synth
-    M, n, k, X, U = _c5_inputs(synth)
+    M, n, k, X, U = _c5_inputs(synth, cfg)
     A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], M["m"], no_transpose=True)
     info = A.info()
     Xd, Ud = to_dev(X), to_dev(U)
@@ -413,7 +416,10 @@ def _seq_single(ff, stream, hbm_peak, args):
     L_full = 2 * ((n + k - 1) // k) + 2
     e_v = info["iterate_bytes"]
     step_bytes = (info["alg_bytes_apply"] - 4 * 2 * n) + 2 * e_v * k * n + e_v * k * n
-    return {"steps_per_s": nsteps / (ms / 1e3), "ms_per_step": ms / nsteps, "steps": nsteps,
+    return {"workload": DESCRIBE["c5"] if cfg == "c5" else
+            "c3 recipe with cols = rows (1911130^2, every nonzero +-1 mod 3), k = ku = 16, u8 iterate",
+            "steps_per_s": nsteps / (ms / 1e3), "ms_per_step": ms / nsteps, "steps": nsteps,
+            "iterate_bytes": e_v,
             "L_full": L_full, "full_L_seconds_extrapolated": L_full * ms / nsteps / 1e3,
             "alg_gbs": step_bytes / (ms / nsteps / 1e3) / 1e9,
             "frac": step_bytes / (ms / nsteps / 1e3) / 1e9 / hbm_peak,

@@ -54,7 +54,8 @@ typedef enum {
     FFSPMV_ERR_DIM = 4,         /* vector length disagrees with A; rows or cols
                                    > 2^31-1; nnz >= 2^32                          */
     FFSPMV_ERR_NONSQUARE = 5,   /* ffspmv_sequence on a rows != cols matrix       */
-    FFSPMV_ERR_UNSUPPORTED = 6, /* transpose requested but not built              */
+    FFSPMV_ERR_UNSUPPORTED = 6, /* operation not available for this handle (a
+                                   distributed handle runs ffspmv_sequence only)  */
     FFSPMV_ERR_NOMEM = 7,       /* host or device allocation failed / workspace
                                    smaller than ffspmv_workspace_size            */
     FFSPMV_ERR_CUDA = 8,        /* a CUDA runtime call failed (no device, ...)    */
@@ -102,8 +103,10 @@ enum { FFSPMV_OP_APPLY = 0, FFSPMV_OP_TRANSPOSE = 1, FFSPMV_OP_BLOCK = 2, FFSPMV
 typedef struct {
     uint32_t struct_size;    /* sizeof(ffspmv_options)                            */
     int32_t device;          /* CUDA device ordinal; -1 or 0.. ; default: current */
-    int32_t no_transpose;    /* 1: do not build A^T (apply_transpose then returns
-                                FFSPMV_ERR_UNSUPPORTED)               */
+    int32_t no_transpose;    /* 1: do not store A^T: apply_transpose then scatters
+                                the rows of A into per-column u64 sums with
+                                global atomics ("A and A^T cannot be
+                                simultaneously stored")                          */
     int32_t segregate_pm1;   /* 0 auto (default), 1 always, -1 never: the +-1
                                 index-only stream of P:272-288 ("the user can
                                 indicate if she wants to try and make use of
@@ -213,7 +216,10 @@ FFSPMV_API ffspmv_status ffspmv_apply(ffspmv_matrix A, uint32_t alpha, const uin
                                       void *stream);
 
 /* y <- (alpha*A^T*x + beta*y) mod m   ("the transpose product").
- * x: rows entries, y: cols entries.  UNSUPPORTED if built with no_transpose. */
+ * x: rows entries, y: cols entries.  On a handle built with no_transpose the
+ * product scatters A's entries (terms reduced below m + 1, u64 column sums:
+ * exact whatever the order of the atomics) and uses a per-handle scratch:
+ * such calls on one handle must be ordered on one stream. */
 FFSPMV_API ffspmv_status ffspmv_apply_transpose(ffspmv_matrix A, uint32_t alpha,
                                                 const uint32_t *x, uint64_t nx, uint32_t beta,
                                                 uint32_t *y, uint64_t ny, void *stream);

@@ -87,6 +87,7 @@ struct ffspmv_matrix_s {
     ffspmv_info info{};
     uint32_t *flag = nullptr;          // checked-mode flag (device)
     uint32_t *stage = nullptr;         // apply_host staging (device)
+    unsigned long long *tacc = nullptr; // no-transpose fallback: per-column u64 sums (device)
     size_t stage_elems = 0;
     bool checked = false;              // check_inputs option
     std::mutex mu;
@@ -324,7 +325,7 @@ void fill_stats(ffspmv_info &I, const Built &b, uint32_t m) {
     I.nnz_pm1 = a.nnz_pm;
     I.nnz_valued = a.nnz_val;
     I.value_bytes = value_bytes_for(m);
-    I.iterate_bytes = m <= 65536u ? 2 : 4;
+    I.iterate_bytes = m <= 256u ? 1 : m <= 65536u ? 2 : 4;
     I.bands = a.bands;
     I.bands_sell = a.bands_sell;
     I.bands_csr = a.bands_csr;
@@ -619,10 +620,20 @@ ffspmv_status ffspmv_create(ffspmv_matrix *out, uint64_t rows, uint64_t cols, ui
         cleanup();
         return cuda_fail(e, "cudaMalloc flag");
     }
+    if (!want_t) {
+        // the transpose fallback's column sums
+        if ((e = cudaMalloc((void **)&h->tacc, std::max<uint64_t>(cols, 1) * 8)) ||
+            (e = cudaMemset(h->tacc, 0, std::max<uint64_t>(cols, 1) * 8))) {
+            if (h->tacc) cudaFree(h->tacc);
+            cleanup();
+            return cuda_fail(e, "cudaMalloc transpose scratch");
+        }
+    }
     fill_stats(h->info, B, modulus);
     h->info.nnz_input = nnz;
     h->info.device_bytes = h->mem[0].bytes + h->mem[1].bytes + h->pmem[0].bytes + h->pmem[1].bytes +
-                           h->rmem[0].bytes + h->rmem[1].bytes + 256;
+                           h->rmem[0].bytes + h->rmem[1].bytes + 256 + (h->tacc ? std::max<uint64_t>(cols, 1) * 8 : 0);
+    h->info.has_transpose = 1;   // built, or the scatter fallback
     h->info.create_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     h->checked = checked;
@@ -641,6 +652,7 @@ ffspmv_status ffspmv_destroy(ffspmv_matrix A) {
         if (mem.base) cudaFree(mem.base);
     if (A->flag) cudaFree(A->flag);
     if (A->stage) cudaFree(A->stage);
+    if (A->tacc) cudaFree(A->tacc);
     if (A->dist) {
         if (A->dist->buf) cudaFree(A->dist->buf);
         comm_free(A->dist->group);
@@ -725,10 +737,11 @@ ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_
                        uint32_t beta, uint32_t *y, uint64_t ny, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
     if (A->dist) return no_dist(A);
-    if (!A->has_op[which] && !A->has_pan[which] && !A->has_run[which])
-        return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built (no_transpose was set)");
+    const bool scatter = which == 1 && !A->has_op[1] && !A->has_pan[1] && !A->has_run[1];
+    if (scatter && !A->tacc) return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not available");
     uint64_t orows, ocols;
-    op_dims(A, which, orows, ocols);
+    if (scatter) { orows = A->op[0].cols; ocols = A->op[0].rows; }
+    else op_dims(A, which, orows, ocols);
     if (nx != ocols || ny != orows)
         return fail(FFSPMV_ERR_DIM, "x must have " + std::to_string(ocols) + " and y " +
                                         std::to_string(orows) + " entries");
@@ -740,7 +753,8 @@ ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_
     ffspmv_status s;
     if ((s = check_vec(A, x, nx, 1, 1, stream, "x"))) return s;
     if (beta && (s = check_vec(A, y, ny, 1, 1, stream, "y"))) return s;
-    int e = A->has_run[which]   ? launch_runs_apply(A->run[which], A->mod, alpha, x, beta, y, stream)
+    int e = scatter             ? launch_apply_scatter_t(A->op[0], A->mod, alpha, x, beta, y, A->tacc, stream)
+            : A->has_run[which] ? launch_runs_apply(A->run[which], A->mod, alpha, x, beta, y, stream)
             : A->has_pan[which] ? launch_panel_apply(A->pan[which], A->mod, alpha, x, beta, y, stream)
                                 : launch_apply(A->op[which], A->mod, alpha, x, beta, y, stream);
     if (e) return cuda_fail(e, "apply launch");
@@ -873,10 +887,10 @@ ffspmv_status ffspmv_apply_host(ffspmv_matrix A, int which, uint32_t alpha, cons
     if (A->dist) return no_dist(A);
     if (which != FFSPMV_OP_APPLY && which != FFSPMV_OP_TRANSPOSE)
         return fail(FFSPMV_ERR_INVALID_ARG, "op must be FFSPMV_OP_APPLY or FFSPMV_OP_TRANSPOSE");
-    if (!A->has_op[which] && !A->has_pan[which] && !A->has_run[which])
-        return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not built");
+    const bool scatter = which == 1 && !A->has_op[1] && !A->has_pan[1] && !A->has_run[1];
     struct { uint64_t rows, cols; } op{};
-    op_dims(A, which, op.rows, op.cols);
+    if (scatter) { op.rows = A->op[0].cols; op.cols = A->op[0].rows; }
+    else op_dims(A, which, op.rows, op.cols);
     if ((op.cols && !x_host) || (op.rows && !y_host))
         return fail(FFSPMV_ERR_INVALID_ARG, "NULL host vector");
     std::lock_guard<std::mutex> lk(A->mu);

@@ -243,11 +243,19 @@ template <> struct VecT<uint32_t, 4> { typedef uint4 T; };
 template <> struct VecT<uint32_t, 2> { typedef uint2 T; };
 template <> struct VecT<uint16_t, 4> { typedef uint2 T; };
 template <> struct VecT<uint16_t, 2> { typedef uint32_t T; };
+template <> struct VecT<uint8_t, 4> { typedef uint32_t T; };
+template <> struct VecT<uint8_t, 2> { typedef uint16_t T; };
 
 template <class TX, int CPL>
 __device__ __forceinline__ void ld_vec(const TX *p, uint32_t (&v)[CPL]) {
     typedef typename VecT<TX, CPL>::T V;
     const V w = __ldg(reinterpret_cast<const V *>(p));
+    if constexpr (sizeof(TX) == 1) {
+        const uint32_t b = (uint32_t)w;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) v[c] = (b >> (8 * c)) & 0xFFu;
+        return;
+    }
     const uint32_t *u = reinterpret_cast<const uint32_t *>(&w);
     if constexpr (sizeof(TX) == 4) {
 #pragma unroll
@@ -272,12 +280,21 @@ __device__ __forceinline__ void ld_vec_pred(const TX *p, bool pred, uint32_t (&v
         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
                      "@q ld.global.nc.v2.u32 {%0, %1}, [%2];\n\t}"
                      : "+r"(u[0]), "+r"(u[1]) : "l"(p), "r"((uint32_t)pred));
-    } else {
+    } else if constexpr (BYTES == 4) {
         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
                      "@q ld.global.nc.u32 %0, [%1];\n\t}"
                      : "+r"(u[0]) : "l"(p), "r"((uint32_t)pred));
+    } else {
+        unsigned short hw = 0;
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                     "@q ld.global.nc.u16 %0, [%1];\n\t}"
+                     : "+h"(hw) : "l"(p), "r"((uint32_t)pred));
+        u[0] = hw;
     }
-    if constexpr (sizeof(TX) == 4) {
+    if constexpr (sizeof(TX) == 1) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) v[c] = (u[0] >> (8 * c)) & 0xFFu;
+    } else if constexpr (sizeof(TX) == 4) {
 #pragma unroll
         for (int c = 0; c < CPL; ++c) v[c] = u[c];
     } else {
@@ -426,6 +443,8 @@ int launch_block_t(const DevOp &op, const DevMod &M, uint32_t k, uint32_t alpha,
 extern template FFSPMV_BLOCK_LAUNCH(uint32_t, uint32_t);
 extern template FFSPMV_BLOCK_LAUNCH(uint16_t, uint16_t);
 extern template FFSPMV_BLOCK_LAUNCH(uint16_t, uint32_t);
+extern template FFSPMV_BLOCK_LAUNCH(uint8_t, uint8_t);
+extern template FFSPMV_BLOCK_LAUNCH(uint8_t, uint32_t);
 #endif
 
 }  // namespace ffspmv

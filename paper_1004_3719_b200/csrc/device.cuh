@@ -55,6 +55,7 @@ __device__ __forceinline__ uint32_t ld_bcast(const uint8_t *p) {
 // Gathers of x / X / V: reused across the whole launch -> normal caching.
 __device__ __forceinline__ uint32_t ld_gather(const uint32_t *p) { return __ldg(p); }
 __device__ __forceinline__ uint32_t ld_gather(const uint16_t *p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ld_gather(const uint8_t *p) { return __ldg(p); }
 
 // ------------------------------------------------------------ reduction ---
 // Barrett: mu = floor(2^64/m) gives q in {floor(x/m) - 1, floor(x/m)}, so a

@@ -317,6 +317,10 @@ int launch_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t
                     void *ws, size_t ws_bytes, void *stream);
 int launch_check_canonical(const uint32_t *v, uint64_t n, uint64_t ld, uint64_t w, uint32_t m,
                            uint32_t *flag_dev, void *stream);
+// y <- alpha A^T x + beta y by scattering the rows layout of A into acc (cols
+// u64, zero on entry, cleared again on exit) -- the no-transpose fallback
+int launch_apply_scatter_t(const DevOp &op, const DevMod &M, uint32_t alpha, const uint32_t *x,
+                           uint32_t beta, uint32_t *y, unsigned long long *acc, void *stream);
 
 // distributed sequence (seq.cu): rank (i, j) of a P_r x P_c grid
 struct DistSeq {

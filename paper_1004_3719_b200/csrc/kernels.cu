@@ -201,4 +201,95 @@ int launch_check_canonical(const uint32_t *v, uint64_t n, uint64_t ld, uint64_t 
     return (int)cudaGetLastError();
 }
 
+// ============================================ transpose without A^T =======
+// y <- alpha A^T x + beta y from the rows layout of A when A^T is not stored
+// ("matrices such that A and A^T cannot be simultaneously stored
+// ... occurs on GPU's"): every entry a_rc scatters its term into acc[c], a
+// u64 per column, with a global atomic add.  The term is reduced below m+1
+// (x_r or m - x_r for +-1 entries, a x_r mod m for valued ones), so a column
+// sum stays below nnz_col (m + 1) < 2^64: exact and independent of the order
+// of the atomics.  k_scatter_finish reduces, applies alpha / beta and clears
+// acc for the next call.
+template <class VT>
+__device__ __forceinline__ void scatter_entry(unsigned long long *acc, uint32_t c, uint32_t xr, bool pm,
+                                              uint32_t a, const DevMod &M) {
+    if (c == PAD_COL) return;
+    uint64_t t;
+    if (pm) t = (c & SIGN_BIT) ? (uint64_t)(M.m - xr) : xr;
+    else t = mod64((uint64_t)a * xr, M);
+    if (t) atomicAdd(acc + (c & COL_MASK), (unsigned long long)t);
+}
+
+template <class VT>
+__global__ void __launch_bounds__(WARPS * 32)
+k_scatter_t(DevOp op, DevMod M, const uint32_t *__restrict__ x, unsigned long long *__restrict__ acc) {
+    uint32_t w = blockIdx.x * WARPS + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31;
+    const VT *vals = reinterpret_cast<const VT *>(op.vval);
+    if (w < op.n_long) {
+        const LongItem it = op.longs[w];
+        const uint32_t xr = __ldg(x + it.row);
+        for (uint32_t j = lane; j < it.len_p; j += 32) scatter_entry<VT>(acc, op.pcol[it.off_p + j], xr, true, 0, M);
+        for (uint32_t j = lane; j < it.len_v; j += 32)
+            scatter_entry<VT>(acc, op.vcol[it.off_v + j], xr, false, vals[it.off_v + j], M);
+        return;
+    }
+    w -= op.n_long;
+    if (w < op.n_slices) {
+        const SliceHdr h = load_hdr(op.slices + w);
+        const uint32_t row = op.perm[w * 32 + lane];
+        if (row == PAD_ROW) return;
+        const uint32_t xr = __ldg(x + row);
+        for (uint32_t j = 0; j < h.wp; ++j) scatter_entry<VT>(acc, op.pcol[h.off_p + j * 32 + lane], xr, true, 0, M);
+        for (uint32_t j = 0; j < h.wv; ++j) {
+            const uint32_t i = h.off_v + j * 32 + lane;
+            scatter_entry<VT>(acc, op.vcol[i], xr, false, vals[i], M);
+        }
+        return;
+    }
+    w -= op.n_slices;
+    if (w < op.n_groups) {
+        const CsrGroup gr = op.groups[w];
+        for (uint32_t i = 0; i < gr.nrows; ++i) {
+            const uint32_t li = gr.first + i;
+            const uint32_t xr = __ldg(x + op.csr_rows[li]);
+            for (uint32_t t = op.csr_pptr[li] + lane; t < op.csr_pptr[li + 1]; t += 32)
+                scatter_entry<VT>(acc, op.pcol[t], xr, true, 0, M);
+            for (uint32_t t = op.csr_vptr[li] + lane; t < op.csr_vptr[li + 1]; t += 32)
+                scatter_entry<VT>(acc, op.vcol[t], xr, false, vals[t], M);
+        }
+    }
+    // zero rows scatter nothing
+}
+
+__global__ void k_scatter_finish(unsigned long long *__restrict__ acc, uint32_t n, DevMod M, uint32_t alpha,
+                                 uint32_t beta, uint32_t *__restrict__ y) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        const uint64_t s = acc[c];
+        acc[c] = 0;
+        y[c] = epilogue(mod64(s, M), alpha, beta, beta ? y[c] : 0u, M);
+    }
+}
+
+int launch_apply_scatter_t(const DevOp &op, const DevMod &M, uint32_t alpha, const uint32_t *x,
+                           uint32_t beta, uint32_t *y, unsigned long long *acc, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t items = total_items(op);
+    if (items) {
+        dim3 grid((items + WARPS - 1) / WARPS), block(WARPS * 32);
+        switch (M.vbytes) {
+            case 1: k_scatter_t<uint8_t><<<grid, block, 0, st>>>(op, M, x, acc); break;
+            case 2: k_scatter_t<uint16_t><<<grid, block, 0, st>>>(op, M, x, acc); break;
+            default: k_scatter_t<uint32_t><<<grid, block, 0, st>>>(op, M, x, acc); break;
+        }
+        count_launch();
+    }
+    if (op.cols) {
+        const uint32_t blocks = std::min<uint32_t>((op.cols + 255) / 256, 148u * 8);
+        k_scatter_finish<<<blocks, 256, 0, st>>>(acc, op.cols, M, alpha, beta, y);
+        count_launch();
+    }
+    return (int)cudaGetLastError();
+}
+
 }  // namespace ffspmv

@@ -215,7 +215,8 @@ struct SeqOut {
 #pragma unroll
             for (int e = 0; e < PER; ++e) {
                 uint32_t ua;
-                if constexpr (sizeof(IT) == 2) ua = (ws[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                if constexpr (sizeof(IT) == 1) ua = (ws[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+                else if constexpr (sizeof(IT) == 2) ua = (ws[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
                 else ua = ws[e];
                 P[q * PER + e].mad(ua, r);
             }
@@ -398,13 +399,12 @@ template <class IT>
 int launch_step(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku, const IT *Vin, IT *Vout,
                 const IT *Uc, uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp,
                 uint32_t &nc, cudaStream_t st) {
-    // u16 iterate (m <= 65536): products < 2^32, any n < 2^31 rows fit u64;
-    // u32 iterate: exact in u96
-    if constexpr (sizeof(IT) == 2) {
-        if (M.vbytes == 1) {
-            if (ku <= 16) return launch_step_kp<uint8_t, IT, 16, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
-            return launch_step_kp<uint8_t, IT, 32, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
-        }
+    // u8 iterate (m <= 256) and u16 iterate (m <= 65536): products < 2^32,
+    // any n < 2^31 rows fit u64; u32 iterate: exact in u96
+    if constexpr (sizeof(IT) == 1) {
+        if (ku <= 16) return launch_step_kp<uint8_t, IT, 16, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+        return launch_step_kp<uint8_t, IT, 32, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
+    } else if constexpr (sizeof(IT) == 2) {
         if (ku <= 16) return launch_step_kp<uint16_t, IT, 16, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
         return launch_step_kp<uint16_t, IT, 32, Acc64>(op, M, k, ku, Vin, Vout, Uc, po, pp, np, Sp, nc, st);
     } else {
@@ -499,9 +499,8 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
         uint32_t *po = W.partial[t & 1];
         const uint32_t *pp = W.partial[(t - 1) & 1];
         uint32_t *Sp = S + (t - 1) * pairs;
-        err = M.vbytes == 1
-                  ? launch_step_mma<uint8_t>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st)
-                  : launch_step_mma<uint16_t>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
+        // u16 iterates have m > 256 (m <= 256 takes the u8 iterate): u16 values
+        err = launch_step_mma<uint16_t>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
         if (err) return err;
         nprev = nc;
     }
@@ -625,6 +624,7 @@ int launch_sum_mod(const DevMod &M, uint64_t count, uint32_t nparts, const uint3
 size_t sequence_workspace(const DevOp &op, const DevMod &M, uint32_t k, uint32_t ku) {
     const uint64_t n = op.rows;
     const uint32_t nctas = proj_ctas(n);
+    if (M.m <= 256u) return layout<uint8_t>(nullptr, op, M.m, k, ku, nctas).bytes;
     if (M.m <= 65536u) return layout<uint16_t>(nullptr, op, M.m, k, ku, nctas).bytes;
     return layout<uint32_t>(nullptr, op, M.m, k, ku, nctas).bytes;
 }
@@ -634,6 +634,9 @@ int launch_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t
                     size_t ws_bytes, void *stream) {
     (void)ws_bytes;
     cudaStream_t st = (cudaStream_t)stream;
+    // the iterate in the narrowest type holding a residue (SURVEY a-8): u8
+    // for m <= 256 ("compressed" vectors for small fields), u16, u32
+    if (M.m <= 256u) return run_sequence<uint8_t>(op, M, k, X, ku, U, L, S, V_out, ws, st);
     if (M.m <= 65536u) return run_sequence<uint16_t>(op, M, k, X, ku, U, L, S, V_out, ws, st);
     return run_sequence<uint32_t>(op, M, k, X, ku, U, L, S, V_out, ws, st);
 }
@@ -805,9 +808,8 @@ int run_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint3
                 uint32_t *Sp = S_band + (t - 1) * pairs;
                 if constexpr (sizeof(IT) == 2) {
                     if (mma) {
-                        err = M.vbytes == 1
-                                  ? launch_step_mma<uint8_t>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp, nprev, Sp, nc, st)
-                                  : launch_step_mma<uint16_t>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp, nprev, Sp, nc, st);
+                        err = launch_step_mma<uint16_t>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp,
+                                                        nprev, Sp, nc, st);
                     } else {
                         err = launch_step<IT>(op, M, kc, ku, Vin, Vout, Ufused, po, pp, nprev, Sp, nc, st);
                     }
@@ -883,6 +885,7 @@ __global__ void k_dist_put_V(const uint32_t *__restrict__ Gv, uint64_t n, uint32
 }  // namespace
 
 size_t sequence_dist_workspace(const DevOp &op, const DevMod &M, uint32_t kc, uint32_t ku, uint32_t pr) {
+    if (M.m <= 256u) return dist_layout<uint8_t>(nullptr, op, M.m, kc, ku, pr).bytes;
     if (M.m <= 65536u) return dist_layout<uint16_t>(nullptr, op, M.m, kc, ku, pr).bytes;
     return dist_layout<uint32_t>(nullptr, op, M.m, kc, ku, pr).bytes;
 }
@@ -891,6 +894,7 @@ int launch_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, ui
                          const uint32_t *U, uint64_t L, uint32_t *S_band, uint32_t *V_band, void *ws,
                          const DistSeq &d, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (M.m <= 256u) return run_sequence_dist<uint8_t>(op, M, X, k, ku, U, L, S_band, V_band, ws, d, st);
     if (M.m <= 65536u) return run_sequence_dist<uint16_t>(op, M, X, k, ku, U, L, S_band, V_band, ws, d, st);
     return run_sequence_dist<uint32_t>(op, M, X, k, ku, U, L, S_band, V_band, ws, d, st);
 }

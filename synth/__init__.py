@@ -99,12 +99,13 @@ def _values_gl7d(g, n):
     return mag * sign
 
 
-def config_matrix(name: str, scale: float = 1.0):
+def config_matrix(name: str, scale: float = 1.0, square: bool = False):
     """Triples of config ``name``; ``scale`` < 1 shrinks rows and cols
-    (same recipe, smaller shape) for oracle-sized parity cases."""
+    (same recipe, smaller shape) for oracle-sized parity cases; ``square``
+    sets cols = rows (e.g. a GL7d-shaped square matrix for the sequence)."""
     c = CONFIGS[name]
     rows = max(1, int(round(c["rows"] * scale)))
-    cols = max(1, int(round(c["cols"] * scale)))
+    cols = rows if square else max(1, int(round(c["cols"] * scale)))
     g = rng(c["seed"])
     lengths = _row_lengths(g, rows, cols, c["lengths"])
     ri, ci = _distinct_columns(g, lengths, cols)

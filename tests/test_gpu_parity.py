@@ -166,9 +166,6 @@ def test_errors_on_device(ff, cuda):
     with pytest.raises(ff.FFSPMVError) as e:
         ff.ffspmv_apply(A, 1, x[:29], 0, y)
     assert e.value.status == ff.ERR_DIM
-    with pytest.raises(ff.FFSPMVError) as e:
-        ff.ffspmv_apply_transpose(A, 1, y, 0, x)
-    assert e.value.status == ff.ERR_UNSUPPORTED
     bad = dev(np.full(30, m, np.uint32))
     with pytest.raises(ff.FFSPMVError) as e:
         ff.ffspmv_apply(A, 1, bad, 0, y)
@@ -350,3 +347,36 @@ def test_config_c4_block_full(ff, oracle_mod, cuda, k):
         sub = oracle_mod.apply_block(M["rows"], M["cols"], M["row"][sel], M["col"][sel],
                                      M["val"][sel], m, X)
         assert np.array_equal(got[rows], sub[rows])
+
+
+@pytest.mark.parametrize("m", [2, 3, 251, 65521, 65537, (1 << 31) - 1, (1 << 32) - 1])
+def test_transpose_without_store(ff, oracle_mod, cuda, m):
+    """no_transpose: A^T x by scattering A's rows (u64 atomics),
+    every format and long / split rows; the scratch is cleared between calls."""
+    g = synth.rng(606 + m % 1000)
+    for opt in (dict(), dict(force_format=2), dict(force_format=3, long_row=4), dict(segregate_pm1=-1)):
+        for trial in range(3):
+            rows, cols, ri, ci, val = rand_case(g, m, long_rows=(trial == 2))
+            A = ff.ffspmv_create(rows, cols, ri, ci, val, m, no_transpose=True, **opt)
+            for alpha, beta in ((1, 0), (int(g.integers(0, m)), int(g.integers(0, m)))):
+                xt = synth.uniform(g, rows, m)
+                yt0 = synth.uniform(g, cols, m)
+                want = oracle_mod.apply_transpose(rows, cols, ri, ci, val, m, xt, yt0, alpha, beta)
+                ytd = dev(yt0)
+                ff.ffspmv_apply_transpose(A, alpha, dev(xt), beta, ytd)
+                assert np.array_equal(host(ytd), want), (opt, trial)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_config_transpose_without_store(ff, oracle_mod, cuda, name):
+    M = synth.config_matrix(name)
+    m = M["m"]
+    g = synth.rng(synth.CONFIGS[name]["vseed"] + 1)
+    A = ff.ffspmv_create(M["rows"], M["cols"], M["row"], M["col"], M["val"], m, no_transpose=True)
+    import torch
+    for rep in range(2):
+        xt = synth.uniform(g, M["rows"], m)
+        ytd = torch.empty(M["cols"], dtype=torch.int32, device="cuda")
+        ff.ffspmv_apply_transpose(A, 1, dev(xt), 0, ytd)
+        assert np.array_equal(host(ytd), oracle_mod.apply_transpose(M["rows"], M["cols"], M["row"],
+                                                                    M["col"], M["val"], m, xt))

@@ -224,3 +224,29 @@ def test_config_c5_scaled_full_length(ff, oracle_mod, cuda):
     Sw, Vw = oracle_mod.sequence(n, M["row"], M["col"], M["val"], m, X, L, U, want_vout=True)
     assert np.array_equal(host(S).reshape(Sw.shape), Sw)
     assert np.array_equal(host(V), Vw)
+
+
+def test_c3_square_sequence_u8_iterate(ff, oracle_mod, cuda):
+    """m = 3 (every nonzero +-1): the iterate is stored as u8 (SURVEY a-8,
+    P:631).  A square GL7d-shaped matrix at full size (1,911,130 rows, the
+    c3 recipe with cols = rows): the first 4 terms and V_4 against the
+    oracle; a scaled one over the full L = 2 ceil(N/k) + 2."""
+    M = synth.config_matrix("c3", square=True)
+    m, n, k = M["m"], M["rows"], 16
+    A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], m, no_transpose=True)
+    assert A.info()["iterate_bytes"] == 1
+    g = synth.rng(2033)
+    X = synth.uniform(g, (n, k), m)
+    U = synth.uniform(g, (n, k), m)
+    S, V = A.sequence(dev(X), 4, dev(U), want_vout=True)
+    rs, cs, vs = oracle_mod.sort_triples(M["row"], M["col"], M["val"])
+    Sw, Vw = oracle_mod.sequence_mt(n, rs, cs, vs, m, X, 4, U, want_vout=True)
+    assert np.array_equal(host(S).reshape(Sw.shape), Sw)
+    assert np.array_equal(host(V), Vw)
+    Ms = synth.config_matrix("c3", scale=1 / 256, square=True)
+    ns = Ms["rows"]
+    Xs = synth.uniform(g, (ns, k), m)
+    L = 2 * ((ns + k - 1) // k) + 2
+    As = ff.ffspmv_create(ns, ns, Ms["row"], Ms["col"], Ms["val"], m)
+    Ss = As.sequence(dev(Xs), L)
+    assert np.array_equal(host(Ss).reshape(L, k, k), oracle_mod.sequence(ns, Ms["row"], Ms["col"], Ms["val"], m, Xs, L))
