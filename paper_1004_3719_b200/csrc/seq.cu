@@ -298,6 +298,15 @@ inline bool fused_ok(uint32_t k, uint32_t ku) { return k <= 32 && ku <= 32; }
 inline bool mma_ok(uint32_t m, uint32_t k, uint32_t ku) {
     return m <= 65536u && k % 4 == 0 && k >= 4 && k <= 16 && ku <= 16;
 }
+// byte-iterate kernel with the tensor-core projection: m <= 256, k = 16
+inline bool mma_b_ok(uint32_t m, uint32_t k, uint32_t ku) { return m <= 256u && k == 16 && ku <= 16; }
+// the fused tensor-core step for iterate type IT
+template <class IT>
+inline bool mma_for(uint32_t m, uint32_t k, uint32_t ku) {
+    if constexpr (sizeof(IT) == 1) return mma_b_ok(m, k, ku);
+    else if constexpr (sizeof(IT) == 2) return mma_ok(m, k, ku);
+    else return false;
+}
 constexpr uint32_t MAX_STEP_CTAS_PER_SM = 8;
 
 template <class IT>
@@ -306,7 +315,7 @@ SeqLayout<IT> layout(void *ws, const DevOp &op, uint32_t m, uint32_t k, uint32_t
     const uint64_t n = op.rows;
     char *p = (char *)ws;
     size_t off = 0;
-    const bool mma = sizeof(IT) == 2 && mma_ok(m, k, ku);
+    const bool mma = mma_for<IT>(m, k, ku);
     const uint32_t ucols = mma ? 0 : fused_ok(k, ku) ? kup_for(ku) : ku;
     // fused steps ping-pong two partial buffers of up to maxc CTA rows (the
     // step kernels' grid, or the projection's for S_0); the unfused path
@@ -468,9 +477,40 @@ int launch_step_mma(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32
     return launch_step_mma_t<VT, 4, 16>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
 }
 
+int launch_step_b(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
+                  const uint8_t *Vin, uint8_t *Vout, const uint32_t *U, const uint32_t *ufrag,
+                  uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc,
+                  cudaStream_t st) {
+    auto kern = k_seq_step_b<uint8_t>;
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SMMA_WARPS * 32, 0);
+        occ = std::max(1, std::min<int>(occ, (int)MAX_STEP_CTAS_PER_SM));
+    }
+    const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    const uint32_t nctas = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)num_sms() * occ, (items + SMMA_WARPS - 1) / SMMA_WARPS));
+    kern<<<nctas, SMMA_WARPS * 32, 0, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp);
+    count_launch();
+    nc = nctas;
+    return (int)cudaGetLastError();
+}
+
+// one fused tensor-core step for iterate type IT (u8: the byte kernel; u16:
+// the half-slice / 4-column kernels; m <= 256 always takes the u8 iterate,
+// so u16 iterates carry u16 values)
+template <class IT>
+int launch_step_tc(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
+                   const IT *Vin, IT *Vout, const uint32_t *U, const uint32_t *ufrag, uint32_t *po,
+                   const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc, cudaStream_t st) {
+    if constexpr (sizeof(IT) == 1) return launch_step_b(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+    else return launch_step_mma<uint16_t>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+}
+
+template <class IT>
 int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X, uint32_t ku,
                      const uint32_t *U, uint64_t L, uint32_t *S, uint32_t *V_out,
-                     const SeqLayout<uint16_t> &W, uint32_t nctas, cudaStream_t st) {
+                     const SeqLayout<IT> &W, uint32_t nctas, cudaStream_t st) {
     const uint64_t n = op.rows;
     const uint32_t *Uu = U ? U : X;
     const uint32_t pairs = ku * k;
@@ -479,7 +519,7 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
     {
         uint64_t tot = n * (uint64_t)k;
         uint32_t blocks = (uint32_t)std::min<uint64_t>((tot + 255) / 256, (uint64_t)num_sms() * 8);
-        k_seq_prep<uint16_t><<<std::max<uint32_t>(blocks, 1), 256, 0, st>>>(X, Uu, tot, 0, W.V[0], W.Uc);
+        k_seq_prep<IT><<<std::max<uint32_t>(blocks, 1), 256, 0, st>>>(X, Uu, tot, 0, W.V[0], W.Uc);
         count_launch();
         if (op.n_slices) {
             uint64_t words = (uint64_t)op.n_slices * 256;
@@ -494,13 +534,12 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
     uint32_t nprev = nctas;
     for (uint64_t t = 1; t < L; ++t) {
         uint32_t nc = 0;
-        const uint16_t *Vin = W.V[(t - 1) & 1];
-        uint16_t *Vout = W.V[t & 1];
+        const IT *Vin = W.V[(t - 1) & 1];
+        IT *Vout = W.V[t & 1];
         uint32_t *po = W.partial[t & 1];
         const uint32_t *pp = W.partial[(t - 1) & 1];
         uint32_t *Sp = S + (t - 1) * pairs;
-        // u16 iterates have m > 256 (m <= 256 takes the u8 iterate): u16 values
-        err = launch_step_mma<uint16_t>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
+        err = launch_step_tc<IT>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
         if (err) return err;
         nprev = nc;
     }
@@ -508,8 +547,7 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
                                                    S + (L - 1) * pairs);
     count_launch();
     if (V_out) {
-        if ((err = launch_block_t<uint16_t, uint32_t>(op, M, k, 1u, W.V[(L - 1) & 1], k, 0u, V_out,
-                                                      k, (void *)st)))
+        if ((err = launch_block_t<IT, uint32_t>(op, M, k, 1u, W.V[(L - 1) & 1], k, 0u, V_out, k, (void *)st)))
             return err;
     }
     return (int)cudaGetLastError();
@@ -527,8 +565,8 @@ int run_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X
             return (int)cudaMemcpyAsync(V_out, X, n * (size_t)k * 4, cudaMemcpyDeviceToDevice, st);
         return 0;
     }
-    if constexpr (sizeof(IT) == 2) {
-        if (mma_ok(M.m, k, ku)) return run_sequence_mma(op, M, k, X, ku, U, L, S, V_out, W, nctas, st);
+    if constexpr (sizeof(IT) <= 2) {
+        if (mma_for<IT>(M.m, k, ku)) return run_sequence_mma<IT>(op, M, k, X, ku, U, L, S, V_out, W, nctas, st);
     }
     const bool fused = fused_ok(k, ku);
     const uint32_t ldu = fused ? kup_for(ku) : ku;
@@ -712,7 +750,7 @@ DistLayout<IT> dist_layout(void *ws, const DevOp &op, uint32_t m, uint32_t kc, u
     const uint64_t h = op.rows, npad = op.cols;
     char *p = (char *)ws;
     size_t off = 0;
-    const bool mma = sizeof(IT) == 2 && mma_ok(m, kc, ku);
+    const bool mma = mma_for<IT>(m, kc, ku);
     const bool fused = mma || fused_ok(kc, ku);
     const uint32_t ucols = mma ? 0 : fused_ok(kc, ku) ? kup_for(ku) : ku;
     const uint32_t nctas = proj_ctas(h);
@@ -750,7 +788,7 @@ int run_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint3
         k_dist_band<<<grid, 256, 0, st>>>(X, k, d.c0, kc, Uu, ku, d.row0, h, W.Xb, W.Ub);
         count_launch();
     }
-    const bool mma = sizeof(IT) == 2 && mma_ok(M.m, kc, ku);
+    const bool mma = mma_for<IT>(M.m, kc, ku);
     const bool fused = mma || fused_ok(kc, ku);
     const uint32_t ldu = mma ? ku : fused ? kup_for(ku) : ku;
     if (h && mma && op.n_slices) {
@@ -806,10 +844,10 @@ int run_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint3
                 uint32_t *po = W.partial[t & 1];
                 const uint32_t *pp = W.partial[(t - 1) & 1];
                 uint32_t *Sp = S_band + (t - 1) * pairs;
-                if constexpr (sizeof(IT) == 2) {
+                if constexpr (sizeof(IT) <= 2) {
                     if (mma) {
-                        err = launch_step_mma<uint16_t>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp,
-                                                        nprev, Sp, nc, st);
+                        err = launch_step_tc<IT>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp, nprev,
+                                                 Sp, nc, st);
                     } else {
                         err = launch_step<IT>(op, M, kc, ku, Vin, Vout, Ufused, po, pp, nprev, Sp, nc, st);
                     }

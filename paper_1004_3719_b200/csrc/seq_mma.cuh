@@ -493,4 +493,183 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
     }
 }
 
+// ------------------------------------------------ byte iterate (m <= 256) --
+// k = 16, u8 iterate: one lane per row, its 16 columns gathered with one
+// 16-byte load per nonzero (the iterate is half the bytes of the u16 one:
+// P:631 "compressed" vectors for small fields).  Every addend is at most
+// max(m, (m-1)^2) <= 65025 and a slice row holds at most long_row <= 65535
+// entries, so a row's sum stays below 2^32: one u32 accumulator per column.
+// The projection needs one u8 x u8 MMA per n-tile (single-limb residues).
+__device__ __forceinline__ uint4 gather16b(const uint8_t *__restrict__ V, uint32_t word) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    const uint8_t *p = V + (uint64_t)(word & COL_MASK) * 16;
+    asm volatile("{.reg .pred q; setp.ne.u32 q, %5, %6;\n"
+                 "@q ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];}"
+                 : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+                 : "l"(p), "r"(word), "r"(PAD_COL));
+    return v;
+}
+
+template <class VT>
+__device__ __forceinline__ void seq_slice_b(const DevOp &op, const DevMod &M, uint32_t s,
+                                            const SliceHdr &h, uint32_t lane,
+                                            const uint8_t *__restrict__ Vin,
+                                            uint8_t *__restrict__ Vout,
+                                            const uint32_t *__restrict__ ufrag, uint8_t *vt,
+                                            unsigned long long *p64) {
+    const uint32_t m = M.m, wp = h.wp, wv = h.wv;
+    const uint32_t *pc = op.pcol + h.off_p + lane;
+    const uint32_t *vc = op.vcol + h.off_v + lane;
+    const VT *vv = reinterpret_cast<const VT *>(op.vval) + h.off_v + lane;
+    uint32_t acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0;
+    // +-1 slots: x, or m - x for a -1: (x ^ ~0) + (m + 1) = m - x (mod 2^32)
+    {
+        uint32_t c = wp ? ld_bcast(pc) : PAD_COL;
+        uint32_t w1 = wp > 1 ? ld_bcast(pc + 32) : PAD_COL;
+        uint4 x = gather16b(Vin, c);
+        for (uint32_t j = 0; j < wp; ++j) {
+            const uint32_t w2 = j + 2 < wp ? ld_bcast(pc + (j + 2) * 32) : PAD_COL;
+            const uint4 xn = gather16b(Vin, w1);
+            const uint32_t sm = (c & SIGN_BIT) && c != PAD_COL ? 0xFFFFFFFFu : 0u, sa = sm & (m + 1);
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] += (((xs[i >> 2] >> (8 * (i & 3))) & 0xFFu) ^ sm) + sa;
+            c = w1;
+            x = xn;
+            w1 = w2;
+        }
+    }
+    {
+        uint32_t c = wv ? ld_bcast(vc) : PAD_COL, a = wv ? ld_bcast(vv) : 0u;
+        uint32_t w1 = wv > 1 ? ld_bcast(vc + 32) : PAD_COL, a1 = wv > 1 ? ld_bcast(vv + 32) : 0u;
+        uint4 x = gather16b(Vin, c);
+        for (uint32_t j = 0; j < wv; ++j) {
+            const uint32_t w2 = j + 2 < wv ? ld_bcast(vc + (j + 2) * 32) : PAD_COL;
+            const uint32_t a2 = j + 2 < wv ? ld_bcast(vv + (j + 2) * 32) : 0u;
+            const uint4 xn = gather16b(Vin, w1);
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] += a * ((xs[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+            c = w1;
+            a = a1;
+            x = xn;
+            w1 = w2;
+            a1 = a2;
+        }
+    }
+    // residues -> V_{t+1} (one 16-byte store) and the transposed byte tile
+    // VT[col][row] for the projection
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = mod32_min(acc[i], M);
+    if (lane >= h.nrows) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = 0;
+    } else {
+        const uint32_t row = op.perm[s * 32 + lane];
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = r[4 * q] | r[4 * q + 1] << 8 | r[4 * q + 2] << 16 | r[4 * q + 3] << 24;
+        *reinterpret_cast<uint4 *>(Vout + (uint64_t)row * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) vt[i * 32 + lane] = (uint8_t)r[i];
+    __syncwarp();
+    // projection: U^T V with single-limb residues (the U fragments' low plane)
+    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
+    const uint32_t al[4] = {al4.x, al4.y, al4.z, al4.w};
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+        const uint32_t b = nt * 8 + gid;
+        uint32_t bl[2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) bl[jj] = *reinterpret_cast<const uint32_t *>(vt + b * 32 + tig * 4 + 16 * jj);
+        int ll[4] = {0, 0, 0, 0};   // a slice adds at most 32 * 255^2: s32-exact
+        mma_u8(ll, al, bl);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p64[(nt * 4 + e) * 32 + lane] += (uint32_t)ll[e];
+    }
+    __syncwarp();
+}
+
+// the scalar path of the byte kernel (rows outside SELL slices)
+struct SeqScalarOutB {
+    uint8_t *V;
+    const uint32_t *U;
+    uint32_t k, ku;
+    unsigned long long *pn;
+    __device__ __forceinline__ void put(uint32_t row, uint32_t col, bool colok, uint32_t r,
+                                        const DevMod &) {
+        if (!colok) return;
+        V[(uint64_t)row * k + col] = (uint8_t)r;
+        if (r == 0) return;
+        for (uint32_t a = 0; a < ku; ++a)
+            atomicAdd(pn + a * k + col, (unsigned long long)U[(uint64_t)row * ku + a] * r);
+    }
+};
+
+template <class VT, int KP>
+__device__ __noinline__ void seq_item_scalar_b(const DevOp *__restrict__ opg, const DevMod M, uint32_t w,
+                                               uint32_t lane, uint32_t k, const uint8_t *__restrict__ Vin,
+                                               SeqScalarOutB o) {
+    const DevOp op = *opg;
+    block_item<VT, KP, 8>(op, M, w, lane, k, Vin, k, o);
+}
+
+template <class VT>
+__global__ void __launch_bounds__(SMMA_WARPS * 32, 3)
+k_seq_step_b(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, uint32_t ku,
+             const uint8_t *__restrict__ Vin, uint8_t *__restrict__ Vout, const uint32_t *__restrict__ U,
+             const uint32_t *__restrict__ ufrag, uint32_t *__restrict__ part_out,
+             const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev) {
+    __shared__ __align__(16) uint8_t vts[SMMA_WARPS][32 * 32];
+    __shared__ unsigned long long pn[16 * SMMA_KMAX];
+    __shared__ unsigned long long p64s[SMMA_WARPS][SMMA_P64];
+    __shared__ uint32_t red[SMMA_WARPS][16][SMMA_KMAX];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
+    const uint32_t pairs = ku * k;
+    for (uint32_t i = threadIdx.x; i < 16 * SMMA_KMAX; i += SMMA_WARPS * 32) pn[i] = 0;
+    for (uint32_t i = lane; i < SMMA_P64; i += 32) p64s[warp][i] = 0;
+    __syncthreads();
+    for (uint32_t p = gw; part_prev && p < pairs; p += nw) {
+        uint64_t sacc = 0;
+        for (uint32_t c = lane; c < nprev; c += 32) sacc += part_prev[(uint64_t)c * pairs + p];
+        for (int o = 16; o; o >>= 1) sacc += __shfl_xor_sync(0xFFFFFFFFu, sacc, o);
+        if (lane == 0) S_prev[p] = mod64(sacc, M);
+    }
+    unsigned long long *p64 = p64s[warp];
+    SeqScalarOutB sout{Vout, U, k, ku, pn};
+    const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
+    for (uint32_t w = gw; w < items; w += nw) {
+        if (w >= op.n_long && w - op.n_long < op.n_slices) {
+            const uint32_t s = w - op.n_long;
+            const SliceHdr h = load_hdr_b(op.slices + s);
+            seq_slice_b<VT>(op, M, s, h, lane, Vin, Vout, ufrag, vts[warp], p64);
+        } else {
+            seq_item_scalar_b<VT, 16>(opdev, M, w, lane, k, Vin, sout);
+        }
+    }
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t a = gid + 8 * (e >> 1), b = nt * 8 + tig * 2 + (e & 1);
+            red[warp][a][b] = mod64(p64[(nt * 4 + e) * 32 + lane], M);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < pairs; i += SMMA_WARPS * 32) {
+        const uint32_t a = i / k, b = i - a * k;
+        uint64_t sacc = mod64(pn[a * k + b], M);
+#pragma unroll
+        for (int w = 0; w < SMMA_WARPS; ++w) sacc += red[w][a][b];
+        part_out[(uint64_t)blockIdx.x * pairs + i] = mod64(sacc, M);
+    }
+}
+
 }  // namespace ffspmv

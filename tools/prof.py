@@ -25,7 +25,7 @@ a = ap.parse_args()
 if a.lib:
     ff.load(a.lib)
 
-M = synth.config_matrix(a.config)
+M = synth.config_matrix("c3", square=True) if a.config == "c3sq" else synth.config_matrix(a.config)
 m, rows, cols = M["m"], M["rows"], M["cols"]
 A = ff.ffspmv_create(rows, cols, M["row"], M["col"], M["val"], m, no_transpose=a.op != "transpose")
 print(A.info(), flush=True)

@@ -23,7 +23,7 @@ ap.add_argument("--lib", default=None)
 a = ap.parse_args()
 if a.lib:
     ff.load(a.lib)
-M = synth.config_matrix(a.config)
+M = synth.config_matrix("c3", square=True) if a.config == "c3sq" else synth.config_matrix(a.config)
 n, k = M["rows"], a.k
 A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], M["m"], no_transpose=True)
 g = synth.rng(2005)
