@@ -24,7 +24,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU_SOURCES = ["seq.cu", "block.cu", "block16.cu", "block16w.cu", "block8.cu", "kernels.cu", "panel.cu", "runs.cu"]
 CPP_SOURCES = ["abi.cpp", "builder.cpp", "panel_build.cpp", "runs_build.cpp", "comm.cpp"]
-HEADERS = ["internal.hpp", "device.cuh", "block.cuh", "seq_mma.cuh", "comm.hpp"]
+HEADERS = ["internal.hpp", "device.cuh", "block.cuh", "seq_mma.cuh", "comm.hpp", "l2window.hpp"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -8,8 +8,10 @@
 //   finalize  S[t][a][b] = sum_cta partial[cta][a][b] mod m
 //   spmm      V_{t+1} = A V_t   (the block kernel of block.cuh, beta = 0)
 #include <algorithm>
+#include <cstdlib>
 
 #include "block.cuh"
+#include "l2window.hpp"
 #include "seq_mma.cuh"
 
 namespace ffspmv {
@@ -532,6 +534,7 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
     if ((err = project<uint32_t>(X, Uu, ku, M, n, k, ku, W.partial[0], nctas, nullptr, st)))
         return err;
     uint32_t nprev = nctas;
+    L2Window win(st, n * (size_t)k * sizeof(IT));
     for (uint64_t t = 1; t < L; ++t) {
         uint32_t nc = 0;
         const IT *Vin = W.V[(t - 1) & 1];
@@ -539,6 +542,7 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
         uint32_t *po = W.partial[t & 1];
         const uint32_t *pp = W.partial[(t - 1) & 1];
         uint32_t *Sp = S + (t - 1) * pairs;
+        win.set(Vin);
         err = launch_step_tc<IT>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
         if (err) return err;
         nprev = nc;
@@ -606,8 +610,10 @@ int run_sequence(const DevOp &op, const DevMod &M, uint32_t k, const uint32_t *X
     if ((err = project<IT>(W.V[0], W.Uc, ldu, M, n, k, ku, W.partial[0], nctas, nullptr, st)))
         return err;
     uint32_t nprev = nctas;
+    L2Window win(st, n * (size_t)k * sizeof(IT));
     for (uint64_t t = 1; t < L; ++t) {
         uint32_t nc = 0;
+        win.set(W.V[(t - 1) & 1]);
         if ((err = launch_step<IT>(op, M, k, ku, W.V[(t - 1) & 1], W.V[t & 1], W.Uc,
                                    W.partial[t & 1], W.partial[(t - 1) & 1], nprev,
                                    S + (t - 1) * pairs, nc, st)))
@@ -836,9 +842,11 @@ int run_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint3
             return err;
         }
         uint32_t nprev = nctas;
+        L2Window win(st, npad * (size_t)kc * sizeof(IT));
         for (uint64_t t = 1; t < L; ++t) {
             uint32_t nc = nprev;
             const IT *Vin = W.V[(t - 1) & 1];
+            win.set(Vin);
             IT *Vout = W.V[t & 1] + d.own * kc;
             if (h) {
                 uint32_t *po = W.partial[t & 1];
