@@ -200,6 +200,20 @@ def grid_shape(world: int, k: int, n: int = 0, nnz: int = 0, iterate_bytes: int 
     return best
 
 
+_COL_GROUPS = {}
+
+
+def _column_groups(base, pr, pc):
+    """The P_c all-gather groups of a P_r x P_c grid over ranks ``base``,
+    created once per (ranks, grid) and reused by later calls (with NCCL each
+    group is a communicator; re-creating them per call would leak them)."""
+    import torch.distributed as dist
+    key = (id(dist.group.WORLD), base, pr, pc)     # a re-initialised world gets new groups
+    if key not in _COL_GROUPS:
+        _COL_GROUPS[key] = [dist.new_group([base[r * pc + jj] for r in range(pr)]) for jj in range(pc)]
+    return _COL_GROUPS[key]
+
+
 def sequence_2d(n, row_idx, col_idx, vals, m, X, L, U, backend, pr, pc, group=None, want_vout=False,
                 on_step=None):
     """2-D sequence on a P_r x P_c grid of ranks (rank = i * P_c + j): rank
@@ -232,7 +246,7 @@ def sequence_2d(n, row_idx, col_idx, vals, m, X, L, U, backend, pr, pc, group=No
     # one all-gather group per column block (every rank creates every group,
     # in the same order, as torch.distributed requires)
     base = dist.get_process_group_ranks(group) if group is not None else list(range(world))
-    col_groups = [dist.new_group([base[r * pc + jj] for r in range(pr)]) for jj in range(pc)]
+    col_groups = _column_groups(tuple(base), pr, pc)
     ri, ci, v = band_triples(row_idx, col_idx, vals, lo, hi)
     A_band = backend.create(hi - lo, n, ri, ci, v, m)
     dev = getattr(backend, "device", torch.device("cpu"))
