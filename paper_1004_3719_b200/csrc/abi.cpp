@@ -109,6 +109,8 @@ ffspmv_status upload(const HostOp &h, DevOp &d, DevMem &mem) {
     d.n_groups = (uint32_t)h.groups.size();
     d.n_split = h.n_split;
     d.n_zero_rows = (uint32_t)h.zero_rows.size();
+    d.acc96 = 0;
+    for (const SliceHdr &sh : h.slices) d.acc96 |= sh.regime == ACC96;
     void *p_slices, *p_perm, *p_pcol, *p_vcol, *p_vval, *p_longs, *p_groups, *p_crow, *p_cpp,
         *p_cvp, *p_zero, *p_sacc, *p_scnt;
     Part parts[] = {

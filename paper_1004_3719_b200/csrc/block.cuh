@@ -11,7 +11,9 @@
 // SELL slices are walked slot-major: the warp loads slot j of all 32 rows with
 // one coalesced load, then each lane takes the (col, value) of each of its NR
 // rows by __shfl_sync and issues NR independent gathers of X -- NR loads in
-// flight per lane instead of a dependent walk per row.
+// flight per lane instead of a dependent walk per row.  When k % 4 == 0 the
+// slices take block_slice_as instead (4 columns per lane, gathers landed in
+// shared memory by cp.async, see there).
 //
 // Results leave through an output policy `Out`:
 //   out.put(row, col, colok, residue)   called exactly once per (row, col)
@@ -303,94 +305,236 @@ __device__ __forceinline__ void ld_vec_pred(const TX *p, bool pred, uint32_t (&v
     }
 }
 
-template <class Acc, class VT, int KPV, int NRMAX, int CPL, class TX, class Out>
-__device__ __forceinline__ void block_slice_vec(const DevOp &op, const DevMod &M, uint32_t s,
-                                                const SliceHdr &h, uint32_t lane, uint32_t k,
-                                                const TX *__restrict__ X, uint32_t ldx,
-                                                Out &out) {
-    using S = SliceShape<KPV, NRMAX>;
+// Asynchronous-copy slice walk (the default vec4 path).  The random X row
+// gathers are latency-bound: served from L2 they need ~100+ KB in flight
+// per SM (tools/gather_bench3.cu), far more than register-landed loads
+// allow next to the NR x CPL accumulators of a lane (a register-landed
+// version of this walk kept ~40 KB in flight at 20 warps/SM: 235 us for c4
+// k = 16 against 139 us here).  Here the gathers land in a per-warp
+// shared-memory ring with cp.async (LDGSTS, zero-filled for padding slots),
+// D slots ahead of the accumulation, and the slot index words (and values)
+// are copied 2D slots ahead into their own rings, so no load result waits
+// in a register: the in-flight bytes are bounded by shared memory (D slots
+// x 32 rows x CPL columns per warp) instead of registers.  Step j of a pass:
+// wait for the copies of step j - D, accumulate slot j from the rings, then
+// issue the gathers of slot j + D (index words from the ring) and the index
+// / value copies of slot j + 2D.  Lanes: KPV lanes per row, CPL = 4 columns per lane, G = 32 / KPV row groups, NR
+// rows per lane per pass.
+template <int D, int NR, class VT>
+struct AsRing {
+    static constexpr uint32_t data_bytes = D * NR * 32 * 16;
+    static constexpr uint32_t bytes = data_bytes + 2 * D * 128 * 2;
+};
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint32_t n) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_v(uint32_t dst, const void *src, uint32_t n) {
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+    else if constexpr (BYTES == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+}
+
+template <class Acc, class VT, int KPV, int NR, int D, class TX, class Out>
+__device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M, uint32_t s,
+                                               const SliceHdr &h, uint32_t lane, uint32_t k,
+                                               const TX *__restrict__ X, uint32_t ldx, Out &out,
+                                               unsigned char *ring, uint32_t fold_every) {
+    static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
+    constexpr bool FOLD = std::is_same<Acc, Acc64F>::value;
+    constexpr int CPL = 4;
+    constexpr int BYTES = CPL * (int)sizeof(TX);
+    constexpr uint32_t G = 32 / KPV;
+    constexpr int PASSES = 32 / (G * NR);
+    using R = AsRing<D, NR, VT>;
+    const uint32_t sdata = (uint32_t)__cvta_generic_to_shared(ring) + lane * 16;
+    const uint32_t siw = (uint32_t)__cvta_generic_to_shared(ring) + R::data_bytes;
+    const uint32_t siv = siw + 2 * D * 128;
+    const uint4 *data = reinterpret_cast<const uint4 *>(ring) + lane;
+    const uint32_t *iw = reinterpret_cast<const uint32_t *>(ring + R::data_bytes);
+    const unsigned char *iv = ring + R::data_bytes + 2 * D * 128;
     const uint32_t g = lane / KPV, cl = lane % KPV;
     const uint32_t m = M.m;
-    const uint32_t *pc = op.pcol + h.off_p + lane;
-    const uint32_t *vc = op.vcol + h.off_v + lane;
-    const VT *vv = reinterpret_cast<const VT *>(op.vval) + h.off_v + lane;
-    const uint32_t wp = h.wp, wv = h.wv;
+    const uint32_t wp = h.wp, wt = h.wp + h.wv;
+    const uint32_t *pcl = op.pcol + h.off_p + lane;
+    const uint32_t *vcl = op.vcol + h.off_v + lane - wp * 32;          // index by slot j >= wp
+    const unsigned char *vbl = reinterpret_cast<const unsigned char *>(op.vval) +
+                               ((uint64_t)h.off_v - wp * 32) * sizeof(VT) + lane * 4;
+    const bool vlane = lane < 8 * sizeof(VT);
     for (uint32_t c0 = 0; c0 < k; c0 += KPV * CPL) {
         const uint32_t col = c0 + cl * CPL;
         const bool colok = col < k;
+        const TX *Xc = X + col;
 #pragma unroll 1
-        for (int pass = 0; pass < S::PASSES; ++pass) {
-            const uint32_t rbase = pass * S::G * S::NR + g;
-            Acc acc[S::NR][CPL];
-            uint32_t cw = wp ? ld_bcast(pc) : PAD_COL;
-            for (uint32_t j = 0; j < wp; ++j) {
-                const uint32_t cur = cw;
-                if (j + 1 < wp) cw = ld_bcast(pc + (j + 1) * 32);
-                uint32_t xv[S::NR][CPL], cs[S::NR];
+        for (int pass = 0; pass < PASSES; ++pass) {
+            const uint32_t rbase = pass * G * NR + g;
+            // copies of slot j: its index word / value bytes into idx ring
+            // (j mod 2D), its rows into data ring (j mod D)
+            auto copy_idx = [&](uint32_t j) {
+                const uint32_t q = (j & (2 * D - 1)) * 128;
+                cp_async4(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
+                if (j >= wp && vlane) cp_async4(siv + q + lane * 4, vbl + (uint64_t)j * 32 * sizeof(VT), 4);
+            };
+            auto copy_data = [&](uint32_t j) {
+                const uint32_t *w = iw + (j & (2 * D - 1)) * 32 + rbase;
+                const uint32_t dst = sdata + (j & (D - 1)) * (NR * 512);
 #pragma unroll
-                for (int i = 0; i < S::NR; ++i) {
-                    cs[i] = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
-                    ld_vec_pred<TX, CPL>(X + ((cs[i] & COL_MASK) * ldx + col),
-                                         cs[i] != PAD_COL && colok, xv[i]);
+                for (int i = 0; i < NR; ++i) {
+                    const uint32_t c = w[i * G];
+                    const bool ok = c != PAD_COL && colok;
+                    cp_async_v<BYTES>(dst + i * 512, Xc + (ok ? (c & COL_MASK) * ldx : 0u), ok ? BYTES : 0);
                 }
+            };
+            Acc acc[NR][CPL];
+            auto consume = [&](uint32_t j) {
+                const uint4 *d = data + (j & (D - 1)) * (NR * 32);
+                const uint32_t q = j & (2 * D - 1);
 #pragma unroll
-                for (int i = 0; i < S::NR; ++i)
+                for (int i = 0; i < NR; ++i) {
+                    const uint4 v = d[i * 32];
+                    const uint32_t xv[4] = {v.x, v.y, v.z, v.w};
+                    uint32_t xs[CPL];
+                    if constexpr (sizeof(TX) == 4) {
 #pragma unroll
-                    for (int c = 0; c < CPL; ++c)
-                        acc[i][c].add((cs[i] & SIGN_BIT) ? m - xv[i][c] : xv[i][c]);
-            }
-            uint32_t vw = wv ? ld_bcast(vc) : PAD_COL;
-            uint32_t aw = wv ? ld_bcast(vv) : 0u;
-            for (uint32_t j = 0; j < wv; ++j) {
-                const uint32_t cur = vw, cura = aw;
-                if (j + 1 < wv) { vw = ld_bcast(vc + (j + 1) * 32); aw = ld_bcast(vv + (j + 1) * 32); }
-                uint32_t xv[S::NR][CPL], as[S::NR];
+                        for (int c = 0; c < CPL; ++c) xs[c] = xv[c];
+                    } else if constexpr (sizeof(TX) == 1) {
 #pragma unroll
-                for (int i = 0; i < S::NR; ++i) {
-                    const uint32_t c = __shfl_sync(0xFFFFFFFFu, cur, rbase + i * S::G);
-                    as[i] = __shfl_sync(0xFFFFFFFFu, cura, rbase + i * S::G);
-                    ld_vec_pred<TX, CPL>(X + (c * ldx + col), c != PAD_COL && colok, xv[i]);
+                        for (int c = 0; c < CPL; ++c) xs[c] = (xv[0] >> (8 * c)) & 0xFFu;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) xs[c] = (xv[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                    }
+                    const uint32_t r = rbase + i * G;
+                    if (j < wp) {
+                        // -1: (x ^ ~0) + (m + 1) = m - x (mod 2^32)
+                        const uint32_t sm = (uint32_t)((int32_t)iw[q * 32 + r] >> 31), sa = sm & (m + 1);
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) acc[i][c].add((xs[c] ^ sm) + sa);
+                    } else {
+                        const uint32_t a = reinterpret_cast<const VT *>(iv + q * 128)[r];
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) acc[i][c].mad(a, xs[c]);
+                    }
                 }
+            };
+            auto wait_sync = [&]() {
+                asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+                __syncwarp();
+            };
+            auto commit = []() { asm volatile("cp.async.commit_group;" ::: "memory"); };
+            uint32_t since_fold = 0;
+            auto maybe_fold = [&]() {
+                if constexpr (FOLD) {
+                    if (++since_fold == fold_every) {
+                        since_fold = 0;
 #pragma unroll
-                for (int i = 0; i < S::NR; ++i)
+                        for (int i = 0; i < NR; ++i)
 #pragma unroll
-                    for (int c = 0; c < CPL; ++c) acc[i][c].mad(as[i], xv[i][c]);
+                            for (int c = 0; c < CPL; ++c) acc[i][c].fold(M.r32);
+                    }
+                }
+            };
+            // prologue: index words of slots 0 .. 2D-1, gathers of slots 0 .. D-1
+            for (uint32_t t = 0; t < 2 * D; ++t) {
+                if (t >= (uint32_t)D) {
+                    wait_sync();
+                    if (t - D < wt) copy_data(t - D);
+                }
+                if (t < wt) copy_idx(t);
+                commit();
+            }
+            // steady state: consume j, gathers of j + D, index words of j + 2D
+            uint32_t j = 0;
+#pragma unroll 1
+            for (; j + 2 * D < wt; ++j) {
+                wait_sync();
+                consume(j);
+                maybe_fold();
+                __syncwarp();
+                copy_idx(j + 2 * D);
+                copy_data(j + D);
+                commit();
+            }
+#pragma unroll 1
+            for (; j < wt; ++j) {
+                wait_sync();
+                consume(j);
+                maybe_fold();
+                __syncwarp();
+                if (j + D < wt) copy_data(j + D);
+                commit();
             }
 #pragma unroll
-            for (int i = 0; i < S::NR; ++i) {
-                const uint32_t r = rbase + i * S::G;
+            for (int i = 0; i < NR; ++i) {
+                const uint32_t r = rbase + i * G;
                 if (r < h.nrows) {
                     const uint32_t row = op.perm[s * 32 + r];
 #pragma unroll
                     for (int c = 0; c < CPL; ++c) out.put(row, col + c, colok, acc[i][c].reduce(M), M);
                 }
             }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
         }
     }
 }
 
-// Vector kernel: slices take the CPL path with KPV lanes per row; the rare
-// long rows / CSR groups / zero rows keep the scalar path (KP lanes per row).
-// Occupancy bound per width (measured, tools/time_block.py at c4, m = 2^31-1):
-// 8 CTAs/SM (64 registers) for k <= 8, 5 CTAs/SM (96 registers) above; the
-// few spills cost less than the latency the extra warps hide on the X gathers.
-template <class VT, int KPV, int CPL, int KP, class TX, class TY>
-__global__ void __launch_bounds__(BWARPS * 32, (KP <= 8 ? 8 : 5))
-k_block_vec(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint32_t ldx,
-            BlockOut<TY> out) {
+// D and the occupancy bound: measured on c4 (tools/time_block.py, A/B builds
+// of tools/build_variant_flags.sh): D = 2 at 6 CTAs/SM 88.6 / 139 / 270 us
+// for k = 8 / 16 / 32 against D = 4 (88.1 / 188 / 285) and D = 2 at 8
+// CTAs/SM (90.1 / 166 / 302).
+#ifndef FFSPMV_BLOCK_AS_D
+#define FFSPMV_BLOCK_AS_D 2     // slots in flight per warp (block_slice_as)
+#endif
+#ifndef FFSPMV_BLOCK_MINB
+#define FFSPMV_BLOCK_MINB 6     // resident 4-warp CTAs per SM the register budget is sized for
+#endif
+
+// SELL slices only (warp w = slice w); the other items go to k_block_rest,
+// so their register needs do not constrain this kernel's occupancy.  NR:
+// rows per lane per pass (NR x 4 accumulators).
+template <class Acc, class VT, int KPV, int NR, class TX, class TY>
+__global__ void __launch_bounds__(BWARPS * 32, FFSPMV_BLOCK_MINB)
+k_block_as(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint32_t ldx,
+           BlockOut<TY> out, uint32_t fold_every) {
+    constexpr int D = FFSPMV_BLOCK_AS_D;
+    extern __shared__ __align__(16) unsigned char as_smem[];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t s = blockIdx.x * BWARPS + warp;
+    if (s >= op.n_slices) return;
+    const SliceHdr h = load_hdr_b(op.slices + s);
+    block_slice_as<Acc, VT, KPV, NR, D>(op, M, s, h, threadIdx.x & 31, k, X, ldx, out,
+                                        as_smem + warp * AsRing<D, NR, VT>::bytes, fold_every);
+}
+
+// Every item except the SELL slices: long rows, CSR / COO_S groups, zero rows.
+template <class VT, int KP, class TX, class TY>
+__global__ void __launch_bounds__(BWARPS * 32)
+k_block_rest(DevOp op, DevMod M, uint32_t k, const TX *__restrict__ X, uint32_t ldx,
+             BlockOut<TY> out) {
     uint32_t w = blockIdx.x * BWARPS + (threadIdx.x >> 5);
-    const uint32_t lane = threadIdx.x & 31;
-    if (w >= op.n_long && w - op.n_long < op.n_slices) {
-        const uint32_t s = w - op.n_long;
-        const SliceHdr h = load_hdr_b(op.slices + s);
-        switch (h.regime) {
-            case ACC32: block_slice_vec<Acc32, VT, KPV, 8, CPL>(op, M, s, h, lane, k, X, ldx, out); break;
-            case ACC64: block_slice_vec<Acc64, VT, KPV, 8, CPL>(op, M, s, h, lane, k, X, ldx, out); break;
-            default: block_slice_vec<Acc96, VT, KPV, 4, CPL>(op, M, s, h, lane, k, X, ldx, out); break;
-        }
-        return;
+    if (w >= op.n_long) w += op.n_slices;
+    block_item<VT, KP, 16>(op, M, w, threadIdx.x & 31, k, X, ldx, out);
+}
+
+template <class Acc, class VT, int KPV, int NR, class TX, class TY>
+static void launch_as(dim3 grid, dim3 block, cudaStream_t st, const DevOp &op, const DevMod &M,
+                      uint32_t k, const TX *X, uint32_t ldx, BlockOut<TY> out, uint32_t fold_every = 0) {
+    constexpr int D = FFSPMV_BLOCK_AS_D;
+    const int smem = BWARPS * AsRing<D, NR, VT>::bytes;
+    auto kern = k_block_as<Acc, VT, KPV, NR, TX, TY>;
+    static uint64_t configured = 0;   // per instantiation: devices whose attribute is set
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(configured >> (dev & 63) & 1)) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured |= 1ull << (dev & 63);
     }
-    block_item<VT, KP, 16>(op, M, w, lane, k, X, ldx, out);
+    kern<<<grid, block, smem, st>>>(op, M, k, X, ldx, out, fold_every);
 }
 
 template <class VT, class TX, class TY>
@@ -400,10 +544,31 @@ static void launch_block_vt(dim3 grid, dim3 block, cudaStream_t st, const DevOp 
     const bool vec4 = k >= 8 && k % 4 == 0 && ldx % 4 == 0 &&
                       ((uintptr_t)X % (4 * sizeof(TX))) == 0;
     if (vec4) {
-        if (k <= 8) k_block_vec<VT, 2, 4, 8, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
-        else if (k <= 16) k_block_vec<VT, 4, 4, 16, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
-        else if (k <= 32) k_block_vec<VT, 8, 4, 32, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
-        else k_block_vec<VT, 16, 4, 32, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);
+        const uint32_t rest = total_items_b(op) - op.n_slices;
+        const dim3 gs((op.n_slices + BWARPS - 1) / BWARPS), gr((rest + BWARPS - 1) / BWARPS);
+        if (rest) {
+            if (k <= 8) k_block_rest<VT, 8, TX, TY><<<gr, block, 0, st>>>(op, M, k, X, ldx, out);
+            else if (k <= 16) k_block_rest<VT, 16, TX, TY><<<gr, block, 0, st>>>(op, M, k, X, ldx, out);
+            else k_block_rest<VT, 32, TX, TY><<<gr, block, 0, st>>>(op, M, k, X, ldx, out);
+            count_launch();
+        }
+        if (op.n_slices) {
+            // rows per lane per pass: 32 / G for k <= 16 (one pass), 4 above
+            const uint32_t fe = fold_capacity(M.m, M.r32);
+            if (op.acc96 && fe >= 2) {
+                if (k <= 8) launch_as<Acc64F, VT, 2, 2>(gs, block, st, op, M, k, X, ldx, out, fe);
+                else if (k <= 16) launch_as<Acc64F, VT, 4, 4>(gs, block, st, op, M, k, X, ldx, out, fe);
+                else launch_as<Acc64F, VT, 8, 4>(gs, block, st, op, M, k, X, ldx, out, fe);
+            } else if (op.acc96) {
+                if (k <= 8) launch_as<Acc96, VT, 2, 2>(gs, block, st, op, M, k, X, ldx, out);
+                else if (k <= 16) launch_as<Acc96, VT, 4, 4>(gs, block, st, op, M, k, X, ldx, out);
+                else launch_as<Acc96, VT, 8, 4>(gs, block, st, op, M, k, X, ldx, out);
+            } else {
+                if (k <= 8) launch_as<Acc64, VT, 2, 2>(gs, block, st, op, M, k, X, ldx, out);
+                else if (k <= 16) launch_as<Acc64, VT, 4, 4>(gs, block, st, op, M, k, X, ldx, out);
+                else launch_as<Acc64, VT, 8, 4>(gs, block, st, op, M, k, X, ldx, out);
+            }
+        }
         return;
     }
     if (k <= 1) k_block<VT, 1, TX, TY><<<grid, block, 0, st>>>(op, M, k, X, ldx, out);

@@ -122,14 +122,19 @@ int comm_allgather(CommImpl *c, const void *send, void *recv, size_t bytes, void
         g.send[c->rank] = send;
     }
     g.barrier();
+    // the copies run on the rank's own stream and are drained before the
+    // second barrier: a device-to-device cudaMemcpy may return before the
+    // copy completes, and neither this rank's next kernel (on `st`) nor a
+    // peer overwriting its send buffer may overlap it
     for (int q = 0; q < g.n; ++q) {
         char *dst = (char *)recv + (size_t)q * bytes;
         if (g.send[q] == dst || !bytes) continue;
-        if ((e = (int)cudaMemcpy(dst, g.send[q], bytes, cudaMemcpyDeviceToDevice))) {
+        if ((e = (int)cudaMemcpyAsync(dst, g.send[q], bytes, cudaMemcpyDeviceToDevice, st))) {
             err = "local all-gather: copy";
             break;
         }
     }
+    if (!e && (e = (int)cudaStreamSynchronize(st))) err = "local all-gather: copy";
     g.barrier();
     return e;
 }

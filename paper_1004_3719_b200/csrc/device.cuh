@@ -6,6 +6,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <type_traits>
+
 #include "internal.hpp"
 
 namespace ffspmv {
@@ -122,6 +125,34 @@ struct Acc96 {
     }
     __device__ __forceinline__ uint32_t reduce(const DevMod &M) const { return mod96(h, lo, M); }
 };
+
+// u64 carrier folded every `fold_every` addends (block_slice_as): after a
+// fold s = hi (2^32 mod m) + lo < 2^32 (r32 + 1), and the host picks
+// fold_every so that many addends of at most (m-1)^2 cannot overflow 2^64
+// (fold_capacity).  One IMAD.WIDE per product instead of u96 carry chains;
+// used when 2^32 mod m is small (e.g. m = 2^31 - 1: r32 = 2, 3 products).
+struct Acc64F {
+    static constexpr bool kFold = true;
+    uint64_t s;
+    __device__ __forceinline__ Acc64F() : s(0) {}
+    __device__ __forceinline__ void add(uint32_t v) { s += v; }
+    __device__ __forceinline__ void mad(uint32_t a, uint32_t x) { s += (uint64_t)a * x; }
+    __device__ __forceinline__ void fold(uint32_t r32) {
+        s = (uint64_t)(uint32_t)(s >> 32) * r32 + (uint32_t)s;
+    }
+    __device__ __forceinline__ uint32_t reduce(const DevMod &M) const { return mod64(s, M); }
+};
+
+// Addends of at most max((m-1)^2, m) an Acc64F can take between folds.
+static inline uint32_t fold_capacity(uint32_t m, uint32_t r32) {
+    const unsigned __int128 top = ((unsigned __int128)1 << 64) - 1;
+    const unsigned __int128 base = ((unsigned __int128)(r32 + 1ull)) << 32;
+    const unsigned __int128 add = std::max<unsigned __int128>((unsigned __int128)(m - 1ull) * (m - 1ull), m);
+    if (base >= top) return 0;
+    const unsigned __int128 f = (top - base) / add;
+    return f > (1u << 30) ? (1u << 30) : (uint32_t)f;
+}
+
 
 // y' = (alpha*r + beta*y) mod m; alpha, beta already reduced mod m; beta == 0
 // means y is not read by the caller.

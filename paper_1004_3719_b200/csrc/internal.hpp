@@ -79,6 +79,7 @@ struct DevOp {
     uint32_t rows, cols;
     uint32_t n_slices, n_long, n_groups, n_split;
     uint32_t n_zero_rows;          // rows of COO_S bands with no entries
+    uint32_t acc96;                // 1: some SELL slice needs the u96 regime
     const SliceHdr *slices;
     const uint32_t *perm;          // slice lane -> row (PAD_ROW for dead lanes)
     const uint32_t *pcol;          // +-1 stream: col | sign, PAD_COL pads
