@@ -451,15 +451,17 @@ int launch_step_h_t(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32
                     uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc,
                     cudaStream_t st) {
     auto kern = k_seq_step_h<VT, LPR>;
+    const int dsmem = FFSPMV_SEQ_AS ? SMMA_WARPS * (int)SeqRing<LPR>::bytes : 0;
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SMMA_WARPS * 32, 0);
+        if (dsmem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SMMA_WARPS * 32, dsmem);
         occ = std::max(1, std::min<int>(occ, (int)MAX_STEP_CTAS_PER_SM));
     }
     const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
     const uint32_t nctas = (uint32_t)std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)num_sms() * occ, (items + SMMA_WARPS - 1) / SMMA_WARPS));
-    kern<<<nctas, SMMA_WARPS * 32, 0, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp);
+    kern<<<nctas, SMMA_WARPS * 32, dsmem, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp);
     count_launch();
     nc = nctas;
     return (int)cudaGetLastError();

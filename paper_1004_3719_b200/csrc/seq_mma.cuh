@@ -427,6 +427,183 @@ __device__ __forceinline__ void seq_slice_h(const DevOp &op, const DevMod &M, ui
     __syncwarp();
 }
 
+// cp.async variant of seq_slice_h (the default for k in {8, 16}): the same
+// lane map (LPR lanes per row, 8 iterate columns = one 16-byte gather per
+// lane and nonzero) but all LPR passes at once (NR = LPR rows per lane) and
+// the gathers landed in a per-warp shared-memory ring D slots ahead of the
+// accumulation, the slot index words / values 2D slots ahead (as in
+// block_slice_as: no in-flight load waits in a register, so the bytes in
+// flight are bounded by shared memory, not by the accumulators' registers).
+// The residues, V_{t+1} stores and the MMA projection are those of
+// seq_slice_h.
+#ifndef FFSPMV_SEQ_AS_D
+#define FFSPMV_SEQ_AS_D 2
+#endif
+template <int LPR>
+struct SeqRing {
+    static constexpr int D = FFSPMV_SEQ_AS_D;
+    static constexpr uint32_t data_bytes = D * LPR * 32 * 16;
+    static constexpr uint32_t bytes = data_bytes + 2 * D * 128 * 2;
+};
+
+template <class VT, int LPR>
+__device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, uint32_t s,
+                                             const SliceHdr &h, uint32_t lane, uint32_t k,
+                                             const uint16_t *__restrict__ Vin,
+                                             uint16_t *__restrict__ Vout,
+                                             const uint32_t *__restrict__ ufrag, uint8_t *vt,
+                                             unsigned long long *p64, unsigned char *ring) {
+    constexpr int D = SeqRing<LPR>::D;
+    constexpr int NR = LPR;                 // rows per lane (one pass over the slice)
+    constexpr uint32_t RPP = 32 / LPR;      // rows per lane group
+    static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(ring);
+    const uint32_t sdata = sbase + lane * 16;
+    const uint32_t siw = sbase + SeqRing<LPR>::data_bytes, siv = siw + 2 * D * 128;
+    const uint4 *data = reinterpret_cast<const uint4 *>(ring) + lane;
+    const uint32_t *iw = reinterpret_cast<const uint32_t *>(ring + SeqRing<LPR>::data_bytes);
+    const unsigned char *iv = ring + SeqRing<LPR>::data_bytes + 2 * D * 128;
+    const uint32_t m = M.m, wp = h.wp, wt = h.wp + h.wv;
+    const uint32_t c0 = (lane % LPR) * 8, g = lane / LPR;
+    const bool colok = c0 < k;
+    const uint16_t *Vc = Vin + c0;
+    const uint32_t *pcl = op.pcol + h.off_p + lane;
+    const uint32_t *vcl = op.vcol + h.off_v + lane - wp * 32;
+    const unsigned char *vbl = reinterpret_cast<const unsigned char *>(op.vval) +
+                               ((uint64_t)h.off_v - wp * 32) * sizeof(VT) + lane * 4;
+    const bool vlane = lane < 8 * sizeof(VT);
+    uint32_t a32[NR][8];
+    unsigned long long a64[NR][8];
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) { a32[i][c] = 0; a64[i][c] = 0; }
+    auto copy_idx = [&](uint32_t j) {
+        const uint32_t q = (j & (2 * D - 1)) * 128;
+        cp_async4(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
+        if (j >= wp && vlane) cp_async4(siv + q + lane * 4, vbl + (uint64_t)j * 32 * sizeof(VT), 4);
+    };
+    auto copy_data = [&](uint32_t j) {
+        const uint32_t *w = iw + (j & (2 * D - 1)) * 32 + g;
+        const uint32_t dst = sdata + (j & (D - 1)) * (NR * 512);
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const uint32_t c = w[i * RPP];
+            const bool ok = c != PAD_COL && colok;
+            cp_async_v<16>(dst + i * 512, Vc + (ok ? (c & COL_MASK) * k : 0u), ok ? 16u : 0u);
+        }
+    };
+    auto consume = [&](uint32_t j) {
+        const uint4 *d = data + (j & (D - 1)) * (NR * 32);
+        const uint32_t q = j & (2 * D - 1);
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const uint4 v = d[i * 32];
+            const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
+            const uint32_t r = i * RPP + g;
+            if (j < wp) {
+                // -1: (x ^ ~0) + (m + 1) = m - x (mod 2^32)
+                const uint32_t sm = (uint32_t)((int32_t)iw[q * 32 + r] >> 31), sa = sm & (m + 1);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    a32[i][2 * c] += ((xs[c] & 0xFFFFu) ^ sm) + sa;
+                    a32[i][2 * c + 1] += ((xs[c] >> 16) ^ sm) + sa;
+                }
+            } else {
+                const uint32_t a = reinterpret_cast<const VT *>(iv + q * 128)[r];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    a64[i][2 * c] += (unsigned long long)a * (xs[c] & 0xFFFFu);
+                    a64[i][2 * c + 1] += (unsigned long long)a * (xs[c] >> 16);
+                }
+            }
+        }
+    };
+    auto wait_sync = [&]() {
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+        __syncwarp();
+    };
+    auto commit = []() { asm volatile("cp.async.commit_group;" ::: "memory"); };
+    for (uint32_t t = 0; t < 2 * D; ++t) {
+        if (t >= (uint32_t)D) {
+            wait_sync();
+            if (t - D < wt) copy_data(t - D);
+        }
+        if (t < wt) copy_idx(t);
+        commit();
+    }
+    uint32_t j = 0;
+#pragma unroll 1
+    for (; j + 2 * D < wt; ++j) {
+        wait_sync();
+        consume(j);
+        __syncwarp();
+        copy_idx(j + 2 * D);
+        copy_data(j + D);
+        commit();
+    }
+#pragma unroll 1
+    for (; j < wt; ++j) {
+        wait_sync();
+        consume(j);
+        __syncwarp();
+        if (j + D < wt) copy_data(j + D);
+        commit();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    // residues -> V_{t+1} and the transposed limb tile (as seq_slice_h)
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        const uint32_t rl = i * RPP + g;
+        uint32_t r[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) r[c] = mod48(a64[i][c] + a32[i][c], M);
+        if (rl >= h.nrows) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) r[c] = 0;
+        } else if (colok) {
+            const uint32_t row = op.perm[s * 32 + rl];
+            *reinterpret_cast<uint4 *>(Vout + (uint64_t)row * k + c0) =
+                make_uint4(r[0] | r[1] << 16, r[2] | r[3] << 16, r[4] | r[5] << 16, r[6] | r[7] << 16);
+        }
+        if (colok) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                vt[(c0 + c) * 32 + rl] = (uint8_t)(r[c] >> 8);
+                vt[32 * 32 + (c0 + c) * 32 + rl] = (uint8_t)r[c];
+            }
+        }
+    }
+    __syncwarp();
+    const uint4 ah4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256) + lane);
+    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
+    const uint32_t ah[4] = {ah4.x, ah4.y, ah4.z, ah4.w}, al[4] = {al4.x, al4.y, al4.z, al4.w};
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < LPR; ++nt) {
+        const uint32_t b = nt * 8 + gid;
+        uint32_t bh[2], bl[2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const uint32_t off = b * 32 + tig * 4 + 16 * jj;
+            bh[jj] = *reinterpret_cast<const uint32_t *>(vt + off);
+            bl[jj] = *reinterpret_cast<const uint32_t *>(vt + 32 * 32 + off);
+        }
+        int hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
+        mma_u8(hh, ah, bh);
+        mma_u8(cr, ah, bl);
+        mma_u8(cr, al, bh);
+        mma_u8(ll, al, bl);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            p64[(nt * 4 + e) * 32 + lane] += ((unsigned long long)(uint32_t)hh[e] << 16) +
+                                             ((unsigned long long)(uint32_t)cr[e] << 8) +
+                                             (uint32_t)ll[e];
+    }
+    __syncwarp();
+}
+
 // rows outside SELL slices (long rows, CSR / COO_S groups, zero rows): kept
 // out of line so their register needs do not constrain the slice path
 // (reads the operator view from a device copy: taking the address of the
@@ -439,8 +616,14 @@ __device__ __noinline__ void seq_item_scalar(const DevOp *__restrict__ opg, cons
     block_item<VT, KP, 8>(op, M, w, lane, k, Vin, k, o);
 }
 
+#ifndef FFSPMV_SEQ_AS
+#define FFSPMV_SEQ_AS 1          // 1: seq_slice_as (cp.async ring), 0: seq_slice_h
+#endif
+#ifndef FFSPMV_SEQ_MINB
+#define FFSPMV_SEQ_MINB 3
+#endif
 template <class VT, int LPR>
-__global__ void __launch_bounds__(SMMA_WARPS * 32, 3)
+__global__ void __launch_bounds__(SMMA_WARPS * 32, FFSPMV_SEQ_MINB)
 k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, uint32_t ku,
              const uint16_t *__restrict__ Vin,
              uint16_t *__restrict__ Vout, const uint32_t *__restrict__ U,
@@ -469,7 +652,13 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
         if (w >= op.n_long && w - op.n_long < op.n_slices) {
             const uint32_t s = w - op.n_long;
             const SliceHdr h = load_hdr_b(op.slices + s);
-            seq_slice_h<VT, LPR>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], p64);
+            if constexpr (FFSPMV_SEQ_AS) {
+                extern __shared__ __align__(16) unsigned char seq_ring[];
+                seq_slice_as<VT, LPR>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], p64,
+                                      seq_ring + warp * SeqRing<LPR>::bytes);
+            } else {
+                seq_slice_h<VT, LPR>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], p64);
+            }
         } else {
             seq_item_scalar<VT, 8 * LPR>(opdev, M, w, lane, k, Vin, sout);
         }

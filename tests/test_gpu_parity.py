@@ -220,6 +220,30 @@ def test_overflow_adversarial(ff, oracle_mod, cuda):
                                                                   np.array([m - 1, m - 1]), 1, 1))
 
 
+@pytest.mark.parametrize("k", [8, 16, 32])
+@pytest.mark.parametrize("m", [65521, (1 << 31) - 1, (1 << 31) + 11, (1 << 32) - 5])
+def test_block_overflow_adversarial(ff, oracle_mod, cuda, m, k):
+    """Block apply (cp.async slice walk) on rows of R maximal products
+    (m-1)(m-1) and -1 entries with x = m-1, R crossing every fold of the
+    folded u64 accumulator (m = 2^31-1: 4 addends per fold) and the u96
+    regime (m with a large 2^32 mod m), all in one SELL band."""
+    g = synth.rng(m % 1009 + k)
+    rows, cols = 96, 4096
+    ri, ci, val = [], [], []
+    for r in range(rows):
+        R = (r % 48) + 1 if r < 64 else 300 + r
+        c = g.choice(cols, size=R, replace=False).astype(np.uint32)
+        v = np.where(g.random(R) < 0.3, -1, m - 1).astype(np.int64)
+        ri.append(np.full(R, r, np.uint32)); ci.append(c); val.append(v)
+    ri, ci, val = np.concatenate(ri), np.concatenate(ci), np.concatenate(val)
+    X = np.full((cols, k), m - 1, np.uint32)
+    X[::7] = g.integers(0, m, size=(len(X[::7]), k), dtype=np.uint64).astype(np.uint32)
+    A = ff.ffspmv_create(rows, cols, ri, ci, val, m, long_row=4096)
+    Yd = dev(np.zeros((rows, k), np.uint32))
+    ff.ffspmv_apply_block(A, k, 1, dev(X), 0, Yd)
+    assert np.array_equal(host(Yd), oracle_mod.apply_block(rows, cols, ri, ci, val, m, X))
+
+
 @pytest.mark.parametrize("strategy", [2, 3])
 @pytest.mark.parametrize("m", [251, 65521, 65536])
 def test_panel_overflow_adversarial(ff, oracle_mod, cuda, m, strategy):
