@@ -291,6 +291,7 @@ struct SeqLayout {
     uint32_t *partial[2];
     uint32_t *ufrag; // tensor-core path: per slice 256 u32 of U limbs in fragment order
     DevOp *opdev;    // device copy of the operator view (out-of-line scalar path)
+    uint32_t *ctr;   // two work counters of the fused steps (step t uses ctr[t & 1])
     size_t bytes;
 };
 
@@ -336,6 +337,7 @@ SeqLayout<IT> layout(void *ws, const DevOp &op, uint32_t m, uint32_t k, uint32_t
     L.partial[1] = (uint32_t *)(p + off); off += fused ? pb : 0;
     L.ufrag = (uint32_t *)(p + off); off += fb;
     L.opdev = (DevOp *)(p + off); off += align256(sizeof(DevOp));
+    L.ctr = (uint32_t *)(p + off); off += 256;
     L.bytes = off;
     return L;
 }
@@ -449,7 +451,7 @@ template <class VT, int LPR>
 int launch_step_h_t(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
                     const uint16_t *Vin, uint16_t *Vout, const uint32_t *U, const uint32_t *ufrag,
                     uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc,
-                    cudaStream_t st) {
+                    uint32_t *ctr, uint32_t *ctr_next, cudaStream_t st) {
     auto kern = k_seq_step_h<VT, LPR>;
     const int dsmem = FFSPMV_SEQ_AS ? SMMA_WARPS * (int)SeqRing<LPR>::bytes : 0;
     static int occ = 0;
@@ -461,7 +463,8 @@ int launch_step_h_t(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32
     const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
     const uint32_t nctas = (uint32_t)std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)num_sms() * occ, (items + SMMA_WARPS - 1) / SMMA_WARPS));
-    kern<<<nctas, SMMA_WARPS * 32, dsmem, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp);
+    kern<<<nctas, SMMA_WARPS * 32, dsmem, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp,
+                                                ctr, ctr_next);
     count_launch();
     nc = nctas;
     return (int)cudaGetLastError();
@@ -471,10 +474,10 @@ template <class VT>
 int launch_step_mma(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
                     const uint16_t *Vin, uint16_t *Vout, const uint32_t *U, const uint32_t *ufrag,
                     uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc,
-                    cudaStream_t st) {
+                    uint32_t *ctr, uint32_t *ctr_next, cudaStream_t st) {
     // k = 8 / 16: the lean half-slice kernel (16-byte gathers, one row per lane)
-    if (k == 8) return launch_step_h_t<VT, 1>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
-    if (k == 16) return launch_step_h_t<VT, 2>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+    if (k == 8) return launch_step_h_t<VT, 1>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, ctr, ctr_next, st);
+    if (k == 16) return launch_step_h_t<VT, 2>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, ctr, ctr_next, st);
     // remaining mma_ok widths: k = 4 (one lane per row) and k = 12 (four
     // 4-column lanes per row, the last one idle)
     if (k == 4) return launch_step_mma_t<VT, 1, 4>(op, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
@@ -484,17 +487,20 @@ int launch_step_mma(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32
 int launch_step_b(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
                   const uint8_t *Vin, uint8_t *Vout, const uint32_t *U, const uint32_t *ufrag,
                   uint32_t *po, const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc,
-                  cudaStream_t st) {
+                  uint32_t *ctr, uint32_t *ctr_next, cudaStream_t st) {
     auto kern = k_seq_step_b<uint8_t>;
+    const int dsmem = FFSPMV_SEQB_AS ? SMMA_WARPS * (int)SeqRing<1>::bytes : 0;
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SMMA_WARPS * 32, 0);
+        if (dsmem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SMMA_WARPS * 32, dsmem);
         occ = std::max(1, std::min<int>(occ, (int)MAX_STEP_CTAS_PER_SM));
     }
     const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
     const uint32_t nctas = (uint32_t)std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)num_sms() * occ, (items + SMMA_WARPS - 1) / SMMA_WARPS));
-    kern<<<nctas, SMMA_WARPS * 32, 0, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp);
+    kern<<<nctas, SMMA_WARPS * 32, dsmem, st>>>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp,
+                                                ctr, ctr_next);
     count_launch();
     nc = nctas;
     return (int)cudaGetLastError();
@@ -506,9 +512,13 @@ int launch_step_b(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t
 template <class IT>
 int launch_step_tc(const DevOp &op, const DevOp *opdev, const DevMod &M, uint32_t k, uint32_t ku,
                    const IT *Vin, IT *Vout, const uint32_t *U, const uint32_t *ufrag, uint32_t *po,
-                   const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc, cudaStream_t st) {
-    if constexpr (sizeof(IT) == 1) return launch_step_b(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
-    else return launch_step_mma<uint16_t>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, st);
+                   const uint32_t *pp, uint32_t np, uint32_t *Sp, uint32_t &nc, uint32_t *ctr,
+                   uint32_t *ctr_next, cudaStream_t st) {
+    if constexpr (sizeof(IT) == 1)
+        return launch_step_b(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, ctr, ctr_next, st);
+    else
+        return launch_step_mma<uint16_t>(op, opdev, M, k, ku, Vin, Vout, U, ufrag, po, pp, np, Sp, nc, ctr,
+                                         ctr_next, st);
 }
 
 template <class IT>
@@ -520,6 +530,7 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
     const uint32_t pairs = ku * k;
     int err;
     if ((err = (int)cudaMemcpyAsync(W.opdev, &op, sizeof(DevOp), cudaMemcpyHostToDevice, st))) return err;
+    if ((err = (int)cudaMemsetAsync(W.ctr, 0, 8, st))) return err;
     {
         uint64_t tot = n * (uint64_t)k;
         uint32_t blocks = (uint32_t)std::min<uint64_t>((tot + 255) / 256, (uint64_t)num_sms() * 8);
@@ -545,7 +556,8 @@ int run_sequence_mma(const DevOp &op, const DevMod &M, uint32_t k, const uint32_
         const uint32_t *pp = W.partial[(t - 1) & 1];
         uint32_t *Sp = S + (t - 1) * pairs;
         win.set(Vin);
-        err = launch_step_tc<IT>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc, st);
+        err = launch_step_tc<IT>(op, W.opdev, M, k, ku, Vin, Vout, Uu, W.ufrag, po, pp, nprev, Sp, nc,
+                                 W.ctr + (t & 1), W.ctr + ((t + 1) & 1), st);
         if (err) return err;
         nprev = nc;
     }
@@ -749,6 +761,7 @@ struct DistLayout {
     uint32_t *ufrag;
     DevOp *opdev;
     uint32_t *bstart;
+    uint32_t *ctr;
     size_t bytes;
 };
 
@@ -774,6 +787,7 @@ DistLayout<IT> dist_layout(void *ws, const DevOp &op, uint32_t m, uint32_t kc, u
     L.ufrag = (uint32_t *)take(mma ? (size_t)op.n_slices * 256 * 4 : 0);
     L.opdev = (DevOp *)take(sizeof(DevOp));
     L.bstart = (uint32_t *)take((size_t)(pr + 1) * 4);
+    L.ctr = (uint32_t *)take(8);
     L.bytes = off;
     return L;
 }
@@ -790,6 +804,7 @@ int run_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint3
     int err;
     if ((err = (int)cudaMemcpyAsync(W.opdev, &op, sizeof(DevOp), cudaMemcpyHostToDevice, st))) return err;
     if ((err = (int)cudaMemcpyAsync(W.bstart, d.bstart, (d.pr + 1) * 4ull, cudaMemcpyHostToDevice, st))) return err;
+    if ((err = (int)cudaMemsetAsync(W.ctr, 0, 8, st))) return err;
     k_dist_prep<IT><<<grid, 256, 0, st>>>(X, k, d.c0, kc, npad, d.rows_max, W.bstart, W.V[0]);
     count_launch();
     if (h) {
@@ -857,7 +872,7 @@ int run_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, uint3
                 if constexpr (sizeof(IT) <= 2) {
                     if (mma) {
                         err = launch_step_tc<IT>(op, W.opdev, M, kc, ku, Vin, Vout, W.Ub, W.ufrag, po, pp, nprev,
-                                                 Sp, nc, st);
+                                                 Sp, nc, W.ctr + (t & 1), W.ctr + ((t + 1) & 1), st);
                     } else {
                         err = launch_step<IT>(op, M, kc, ku, Vin, Vout, Ufused, po, pp, nprev, Sp, nc, st);
                     }

@@ -628,7 +628,8 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
              const uint16_t *__restrict__ Vin,
              uint16_t *__restrict__ Vout, const uint32_t *__restrict__ U,
              const uint32_t *__restrict__ ufrag, uint32_t *__restrict__ part_out,
-             const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev) {
+             const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev,
+             uint32_t *__restrict__ ctr, uint32_t *__restrict__ ctr_next) {
     __shared__ __align__(16) uint8_t vts[SMMA_WARPS][2 * 32 * 32];
     __shared__ unsigned long long pn[16 * SMMA_KMAX];
     __shared__ unsigned long long p64s[SMMA_WARPS][SMMA_P64];
@@ -637,6 +638,7 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
     const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
     const uint32_t pairs = ku * k;
     for (uint32_t i = threadIdx.x; i < 16 * SMMA_KMAX; i += SMMA_WARPS * 32) pn[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ctr_next = 0;   // the next step's work counter
     for (uint32_t i = lane; i < SMMA_P64; i += 32) p64s[warp][i] = 0;
     __syncthreads();
     for (uint32_t p = gw; part_prev && p < pairs; p += nw) {
@@ -648,7 +650,17 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
     unsigned long long *p64 = p64s[warp];
     SeqScalarOut sout{Vout, U, k, ku, pn};
     const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
-    for (uint32_t w = gw; w < items; w += nw) {
+    // items (long rows first, then slices, groups, zero rows) are taken
+    // dynamically from a per-step counter: a warp holding a long row or a
+    // wide slice takes fewer items (the skewed GL7d rows left the static
+    // round-robin split waiting at the final barrier); the next item's
+    // atomic is issued before the current item and read after it
+    uint32_t w = 0;
+    if (lane == 0) w = atomicAdd(ctr, 1u);
+    w = __shfl_sync(0xFFFFFFFFu, w, 0);
+    while (w < items) {
+        uint32_t wn = 0;
+        if (lane == 0) wn = atomicAdd(ctr, 1u);
         if (w >= op.n_long && w - op.n_long < op.n_slices) {
             const uint32_t s = w - op.n_long;
             const SliceHdr h = load_hdr_b(op.slices + s);
@@ -662,6 +674,7 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
         } else {
             seq_item_scalar<VT, 8 * LPR>(opdev, M, w, lane, k, Vin, sout);
         }
+        w = __shfl_sync(0xFFFFFFFFu, wn, 0);
     }
     const uint32_t gid = lane >> 2, tig = lane & 3;
 #pragma unroll
@@ -784,6 +797,122 @@ __device__ __forceinline__ void seq_slice_b(const DevOp &op, const DevMod &M, ui
     __syncwarp();
 }
 
+// cp.async variant of seq_slice_b (the default): the lane's 16-byte row
+// gathers land in a per-warp shared ring 2 slots ahead, index words / values
+// 4 slots ahead (see seq_slice_as).
+template <class VT>
+__device__ __forceinline__ void seq_slice_b_as(const DevOp &op, const DevMod &M, uint32_t s,
+                                               const SliceHdr &h, uint32_t lane,
+                                               const uint8_t *__restrict__ Vin,
+                                               uint8_t *__restrict__ Vout,
+                                               const uint32_t *__restrict__ ufrag, uint8_t *vt,
+                                               unsigned long long *p64, unsigned char *ring) {
+    constexpr int D = SeqRing<1>::D;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(ring);
+    const uint32_t sdata = sbase + lane * 16;
+    const uint32_t siw = sbase + SeqRing<1>::data_bytes, siv = siw + 2 * D * 128;
+    const uint4 *data = reinterpret_cast<const uint4 *>(ring) + lane;
+    const uint32_t *iw = reinterpret_cast<const uint32_t *>(ring + SeqRing<1>::data_bytes);
+    const unsigned char *iv = ring + SeqRing<1>::data_bytes + 2 * D * 128;
+    const uint32_t m = M.m, wp = h.wp, wt = h.wp + h.wv;
+    const uint32_t *pcl = op.pcol + h.off_p + lane;
+    const uint32_t *vcl = op.vcol + h.off_v + lane - wp * 32;
+    const unsigned char *vbl = reinterpret_cast<const unsigned char *>(op.vval) +
+                               ((uint64_t)h.off_v - wp * 32) * sizeof(VT) + lane * 4;
+    const bool vlane = lane < 8 * sizeof(VT);
+    uint32_t acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0;
+    auto copy_idx = [&](uint32_t j) {
+        const uint32_t q = (j & (2 * D - 1)) * 128;
+        cp_async4(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
+        if (j >= wp && vlane) cp_async4(siv + q + lane * 4, vbl + (uint64_t)j * 32 * sizeof(VT), 4);
+    };
+    auto copy_data = [&](uint32_t j) {
+        const uint32_t c = iw[(j & (2 * D - 1)) * 32 + lane];
+        const bool ok = c != PAD_COL;
+        cp_async_v<16>(sdata + (j & (D - 1)) * 512, Vin + (ok ? (uint64_t)(c & COL_MASK) * 16 : 0u), ok ? 16u : 0u);
+    };
+    auto consume = [&](uint32_t j) {
+        const uint4 v = data[(j & (D - 1)) * 32];
+        const uint32_t q = j & (2 * D - 1);
+        const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
+        if (j < wp) {
+            const uint32_t sm = (uint32_t)((int32_t)iw[q * 32 + lane] >> 31), sa = sm & (m + 1);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] += (((xs[i >> 2] >> (8 * (i & 3))) & 0xFFu) ^ sm) + sa;
+        } else {
+            const uint32_t a = reinterpret_cast<const VT *>(iv + q * 128)[lane];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] += a * ((xs[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+        }
+    };
+    auto wait_sync = [&]() {
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+        __syncwarp();
+    };
+    auto commit = []() { asm volatile("cp.async.commit_group;" ::: "memory"); };
+    for (uint32_t t = 0; t < 2 * D; ++t) {
+        if (t >= (uint32_t)D) {
+            wait_sync();
+            if (t - D < wt) copy_data(t - D);
+        }
+        if (t < wt) copy_idx(t);
+        commit();
+    }
+    uint32_t j = 0;
+#pragma unroll 1
+    for (; j + 2 * D < wt; ++j) {
+        wait_sync();
+        consume(j);
+        __syncwarp();
+        copy_idx(j + 2 * D);
+        copy_data(j + D);
+        commit();
+    }
+#pragma unroll 1
+    for (; j < wt; ++j) {
+        wait_sync();
+        consume(j);
+        __syncwarp();
+        if (j + D < wt) copy_data(j + D);
+        commit();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = mod32_min(acc[i], M);
+    if (lane >= h.nrows) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = 0;
+    } else {
+        const uint32_t row = op.perm[s * 32 + lane];
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = r[4 * q] | r[4 * q + 1] << 8 | r[4 * q + 2] << 16 | r[4 * q + 3] << 24;
+        *reinterpret_cast<uint4 *>(Vout + (uint64_t)row * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) vt[i * 32 + lane] = (uint8_t)r[i];
+    __syncwarp();
+    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
+    const uint32_t al[4] = {al4.x, al4.y, al4.z, al4.w};
+    const uint32_t gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+        const uint32_t b = nt * 8 + gid;
+        uint32_t bl[2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) bl[jj] = *reinterpret_cast<const uint32_t *>(vt + b * 32 + tig * 4 + 16 * jj);
+        int ll[4] = {0, 0, 0, 0};
+        mma_u8(ll, al, bl);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p64[(nt * 4 + e) * 32 + lane] += (uint32_t)ll[e];
+    }
+    __syncwarp();
+}
+
 // the scalar path of the byte kernel (rows outside SELL slices)
 struct SeqScalarOutB {
     uint8_t *V;
@@ -808,12 +937,24 @@ __device__ __noinline__ void seq_item_scalar_b(const DevOp *__restrict__ opg, co
     block_item<VT, KP, 8>(op, M, w, lane, k, Vin, k, o);
 }
 
+#ifndef FFSPMV_SEQB_MINB
+#define FFSPMV_SEQB_MINB 3
+#endif
+// The byte kernel keeps its register-landed gathers: measured on the square
+// GL7d m = 3 sequence (tools/time_seq.py --config c3sq, dynamic item
+// scheduling in both): 0.356 ms/step against 0.385 with the cp.async ring
+// (one 16-byte gather per lane and slot: the ring's per-slot bookkeeping is
+// not amortised, and the 30 MB byte iterate stays L2-resident).
+#ifndef FFSPMV_SEQB_AS
+#define FFSPMV_SEQB_AS 0
+#endif
 template <class VT>
-__global__ void __launch_bounds__(SMMA_WARPS * 32, 3)
+__global__ void __launch_bounds__(SMMA_WARPS * 32, FFSPMV_SEQB_MINB)
 k_seq_step_b(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, uint32_t ku,
              const uint8_t *__restrict__ Vin, uint8_t *__restrict__ Vout, const uint32_t *__restrict__ U,
              const uint32_t *__restrict__ ufrag, uint32_t *__restrict__ part_out,
-             const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev) {
+             const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev,
+             uint32_t *__restrict__ ctr, uint32_t *__restrict__ ctr_next) {
     __shared__ __align__(16) uint8_t vts[SMMA_WARPS][32 * 32];
     __shared__ unsigned long long pn[16 * SMMA_KMAX];
     __shared__ unsigned long long p64s[SMMA_WARPS][SMMA_P64];
@@ -822,6 +963,7 @@ k_seq_step_b(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
     const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
     const uint32_t pairs = ku * k;
     for (uint32_t i = threadIdx.x; i < 16 * SMMA_KMAX; i += SMMA_WARPS * 32) pn[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ctr_next = 0;   // the next step's work counter
     for (uint32_t i = lane; i < SMMA_P64; i += 32) p64s[warp][i] = 0;
     __syncthreads();
     for (uint32_t p = gw; part_prev && p < pairs; p += nw) {
@@ -833,14 +975,31 @@ k_seq_step_b(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
     unsigned long long *p64 = p64s[warp];
     SeqScalarOutB sout{Vout, U, k, ku, pn};
     const uint32_t items = op.n_long + op.n_slices + op.n_groups + (op.n_zero_rows + 31) / 32;
-    for (uint32_t w = gw; w < items; w += nw) {
+    // items (long rows first, then slices, groups, zero rows) are taken
+    // dynamically from a per-step counter: a warp holding a long row or a
+    // wide slice takes fewer items (the skewed GL7d rows left the static
+    // round-robin split waiting at the final barrier); the next item's
+    // atomic is issued before the current item and read after it
+    uint32_t w = 0;
+    if (lane == 0) w = atomicAdd(ctr, 1u);
+    w = __shfl_sync(0xFFFFFFFFu, w, 0);
+    while (w < items) {
+        uint32_t wn = 0;
+        if (lane == 0) wn = atomicAdd(ctr, 1u);
         if (w >= op.n_long && w - op.n_long < op.n_slices) {
             const uint32_t s = w - op.n_long;
             const SliceHdr h = load_hdr_b(op.slices + s);
-            seq_slice_b<VT>(op, M, s, h, lane, Vin, Vout, ufrag, vts[warp], p64);
+            if constexpr (FFSPMV_SEQB_AS) {
+                extern __shared__ __align__(16) unsigned char seq_ring_b[];
+                seq_slice_b_as<VT>(op, M, s, h, lane, Vin, Vout, ufrag, vts[warp], p64,
+                                   seq_ring_b + warp * SeqRing<1>::bytes);
+            } else {
+                seq_slice_b<VT>(op, M, s, h, lane, Vin, Vout, ufrag, vts[warp], p64);
+            }
         } else {
             seq_item_scalar_b<VT, 16>(opdev, M, w, lane, k, Vin, sout);
         }
+        w = __shfl_sync(0xFFFFFFFFu, wn, 0);
     }
     const uint32_t gid = lane >> 2, tig = lane & 3;
 #pragma unroll
