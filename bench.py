@@ -425,7 +425,7 @@ def _seq_single(ff, stream, hbm_peak, args, cfg="c5"):
             "frac": step_bytes / (ms / nsteps / 1e3) / 1e9 / hbm_peak,
             "alg_bytes_per_step": step_bytes,
             "launches_per_step": (ff.ffspmv_kernel_launches() - l0) / nsteps,
-            "traffic": ncu_traffic("c5_sequence_step"),
+            "traffic": ncu_traffic("c5_sequence_step" if cfg == "c5" else "c3sq_sequence_step"),
             "note": "one ffspmv_sequence call of 200 steps (S_0..S_199); L2 not flushed between "
                     "steps (the iterate is reused by design)"}
 

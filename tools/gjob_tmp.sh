@@ -1,6 +1,7 @@
-# scratch gpurun job: round-end check of the committed tree (tests, bench, smoke, launch list)
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; echo "tests rc=$?" >> gpurun_out/gputest.log
-timeout 600 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 3 --warmup 3 --cpu-seconds 0.5 > /dev/null 2>&1
+mkdir -p gpurun_out; rm -f gpurun_out/time_seq.log
+for v in main sbas0; do
+  if [ $v = main ]; then L=""; else L="--lib tools/variants/lib$v.so"; fi
+  timeout 300 python tools/time_seq.py --config c3sq $L >> gpurun_out/time_seq.log 2>&1
+  timeout 300 python tools/time_seq.py $L >> gpurun_out/time_seq.log 2>&1
+done
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -k "sequence or dist or c5 or c3_square" > gpurun_out/t_seq.log 2>&1; echo "rc=$?" >> gpurun_out/t_seq.log

@@ -57,11 +57,14 @@ def main(src, dst):
     md.append("")
     # full captures
     traffic = {}
-    caps = [("c2_apply", "c2 apply (k_panel + k_panel_reduce, one call)"),
-            ("c3_apply", "c3 apply (k_panel + k_panel_reduce, one call)"),
-            ("c4_block16", "c4 block SpMM k = 16 (k_block_vec)"),
-            ("c5_seq", "c5 fused sequence step (k_seq_step_mma)")]
-    for key, title in caps:
+    caps = [("c2_apply", "c2_apply", "c2 apply (k_panel + k_panel_reduce, one call)"),
+            ("c3_apply", "c3_apply", "c3 apply (k_runs_pack + k_runs + k_runs_reduce, one call)"),
+            ("c4_block8", "c4_block_k8", "c4 block SpMM k = 8 (k_block_as)"),
+            ("c4_block16", "c4_block_k16", "c4 block SpMM k = 16 (k_block_as)"),
+            ("c4_block32", "c4_block_k32", "c4 block SpMM k = 32 (k_block_as)"),
+            ("c5_seq", "c5_sequence_step", "c5 fused sequence step (k_seq_step_h, cp.async ring)"),
+            ("c3sq_seq", "c3sq_sequence_step", "square GL7d m = 3 sequence step (k_seq_step_b, u8 iterate)")]
+    for key, tkey, title in caps:
         p = os.path.join(src, f"{key}_raw.csv")
         if not os.path.exists(p):
             continue
@@ -78,7 +81,7 @@ def main(src, dst):
                                                else str(k.get(n, "-")) for k in ks) + " |")
         dram = sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in ks)
         tns = sum(k.get("gpu__time_duration.sum", 0) for k in ks)
-        traffic[key.replace("c4_block16", "c4_block_k16").replace("c5_seq", "c5_sequence_step")] = int(dram)
+        traffic[tkey] = int(dram)
         md += ["", f"DRAM traffic per call: {dram / 1e6:.2f} MB in {tns / 1e3:.1f} µs (ncu, cold caches).", ""]
     with open(os.path.join(dst, "SUMMARY.md"), "w") as f:
         f.write("\n".join(md) + "\n")
