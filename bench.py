@@ -459,7 +459,52 @@ def bench_multi(args, world, rank, local):
                       "modulus": 65521, "parallelism": r.get("parallelism"),
                       "l2": "not flushed between steps (the iterate is reused by design)"},
            "gpu_launches": r.get("launches"), "detail": r}
+    if not args.no_extras:
+        out["extras"] = {"c4_block_k16_row_sharded": _block_dist(args, world)}
     return out
+
+
+def _block_dist(args, world):
+    """c4 block SpMM (k = 16, m = 2^31 - 1) as ONE problem row-sharded over
+    the ranks through a distributed handle (ffspmv_apply_block: each rank its
+    nnz-balanced row band, then the all-gather of the Y bands so Y is whole on
+    every rank); nnz*k/s from device events around each call, max over
+    ranks, L2 not flushed."""
+    import torch
+
+    import paper_1004_3719_b200 as ff
+    import synth
+    try:
+        M = synth.config_matrix("c4")
+        n, k = M["rows"], 16
+        comm = ff.comm_from_torch()
+        A = ff.ffspmv_create(n, n, M["row"], M["col"], M["val"], M["m"], comm=comm, dist_rows=world)
+        g = synth.rng(2004)
+        X = to_dev(synth.uniform(g, (n, k), M["m"]))
+        Y = torch.empty((n, k), dtype=torch.int32, device="cuda")
+        stream = torch.cuda.current_stream()
+        for _ in range(max(3, args.warmup)):
+            ff.ffspmv_apply_block(A, k, 1, X, 0, Y, stream)
+        ts = []
+        for _ in range(max(1, min(args.steps, 20))):
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ff.ffspmv_apply_block(A, k, 1, X, 0, Y, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tt = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ts.append(float(tt.item()))
+        ms = float(np.median(ts))
+        nnz = _canonical_nnz(M)
+        del A
+        comm.close()
+        return {"nnz_k_per_s": nnz * k / (ms / 1e3), "ms": ms, "grid": [world, 1],
+                "note": "row bands of A over the ranks, X replicated, Y all-gathered (included)"}
+    except Exception as e:                       # the line must still print
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def _seq_dist(args, world, rank, local):

@@ -304,9 +304,16 @@ FFSPMV_API ffspmv_status ffspmv_sum_mod(ffspmv_matrix A, uint64_t count, uint32_
  * P:457-460 ("ship independent set of vector blocks ... then gather").
  * ffspmv_sequence takes the same arguments as on one GPU -- X, U (full
  * n x k / n x ku, replicated), S (full L x ku x k) and V_out (full) on every
- * rank -- and returns results identical to the one-GPU call.  Only
- * ffspmv_sequence, ffspmv_workspace_size and ffspmv_get_info accept a
- * distributed handle (the others return FFSPMV_ERR_UNSUPPORTED).  Calls on a
+ * rank -- and returns results identical to the one-GPU call.
+ * ffspmv_apply_block (and ffspmv_apply, its k = 1 case) on a distributed
+ * handle is the row-sharded single product: rank (i, j)
+ * computes Y[band i, block j] = alpha A X + beta Y in place, then the blocks
+ * of all ranks are all-gathered into Y, so Y (replicated on entry, n x k
+ * contiguous: ldx = ldy = k, else FFSPMV_ERR_UNSUPPORTED) is the full
+ * one-GPU result on every rank on return.  ffspmv_sequence,
+ * ffspmv_apply(_block), ffspmv_workspace_size and ffspmv_get_info accept a
+ * distributed handle (the others -- the transpose, apply_host, project,
+ * sum_mod -- return FFSPMV_ERR_UNSUPPORTED).  Calls on a
  * distributed handle must not overlap (it owns the result-exchange buffers,
  * allocated on first use and grown with L). */
 FFSPMV_API ffspmv_status ffspmv_comm_unique_id(void *id_128);

@@ -732,13 +732,81 @@ ffspmv_status check_vec(ffspmv_matrix A, const uint32_t *v, uint64_t n, uint64_t
 }
 
 ffspmv_status no_dist(ffspmv_matrix A) {
-    return fail(FFSPMV_ERR_UNSUPPORTED, "a distributed handle supports ffspmv_sequence only");
+    return fail(FFSPMV_ERR_UNSUPPORTED,
+                "a distributed handle supports ffspmv_sequence, ffspmv_apply and ffspmv_apply_block only");
+}
+
+// Grow the handle's result-exchange buffer (calls on a distributed handle do
+// not overlap).
+ffspmv_status dist_buf(DistState &d, size_t want) {
+    if (want <= d.buf_bytes) return FFSPMV_OK;
+    if (d.buf) cudaFree(d.buf);
+    d.buf = nullptr;
+    d.buf_bytes = 0;
+    if (int e = cudaMalloc(&d.buf, want)) return cuda_fail(e, "cudaMalloc exchange buffers");
+    d.buf_bytes = want;
+    return FFSPMV_OK;
+}
+
+// Row-sharded single product on a distributed handle (SURVEY §8e "single
+// apply / block apply shard naturally"): rank (i, j) computes
+// Y[band i, block j] = alpha A[band i, :] X[:, block j] + beta Y[...] in place
+// in the caller's Y (X scattered once into the band operator's padded column
+// layout), then every rank's block is all-gathered and written into Y, so Y
+// (replicated, n x k contiguous) is identical on every rank and equal to the
+// one-GPU result.  k = 1 is ffspmv_apply.
+ffspmv_status block_dist(ffspmv_matrix A, uint32_t k, uint32_t alpha, const uint32_t *X, uint32_t beta,
+                         uint32_t *Y, void *stream) {
+    DistState &d = *A->dist;
+    const DevOp &op = A->op[0];
+    const uint32_t c0 = (uint32_t)((uint64_t)k * d.j / d.pc);
+    const uint32_t kc = (uint32_t)((uint64_t)k * (d.j + 1) / d.pc) - c0;
+    const uint32_t kcmax = (k + d.pc - 1) / d.pc;
+    const uint64_t npad = op.cols, h = op.rows, row0 = d.bstart[d.i];
+    alpha %= A->m;
+    beta %= A->m;
+    ffspmv_status s;
+    if ((s = check_vec(A, X, d.n, k, k, stream, "X"))) return s;
+    if (beta && (s = check_vec(A, Y, d.n, k, k, stream, "Y"))) return s;
+    const size_t xb = a256(npad * kcmax * 4ull), vslot = (size_t)d.rows_max * kcmax * 4;
+    if ((s = dist_buf(d, xb + a256(vslot) + a256(vslot * d.nranks) + a256(4 * (d.pr + 1))))) return s;
+    uint32_t *Xp = (uint32_t *)d.buf;
+    uint32_t *Vb = (uint32_t *)((char *)d.buf + xb);
+    uint32_t *Gv = (uint32_t *)((char *)Vb + a256(vslot));
+    uint32_t *bdev = (uint32_t *)((char *)Gv + a256(vslot * d.nranks));
+    cudaStream_t st = (cudaStream_t)stream;
+    int e;
+    if ((e = cudaMemcpyAsync(bdev, d.bstart.data(), 4ull * (d.pr + 1), cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "band starts");
+    if (kc) {
+        if ((e = launch_dist_prep_x(X, k, c0, kc, npad, d.rows_max, bdev, Xp, stream)))
+            return cuda_fail(e, "scatter X");
+        if (h && (e = launch_block(op, A->mod, kc, alpha, Xp, kc, beta, Y + row0 * k + c0, k, stream)))
+            return cuda_fail(e, "band block apply");
+        if (h && (e = cudaMemcpy2DAsync(Vb, kcmax * 4ull, Y + row0 * k + c0, k * 4ull, kc * 4ull, h,
+                                        cudaMemcpyDeviceToDevice, st)))
+            return cuda_fail(e, "pack band block");
+    }
+    std::string err;
+    if ((e = comm_allgather(d.world, Vb, Gv, vslot, stream, err)))
+        return fail(e < 0 ? FFSPMV_ERR_NCCL : FFSPMV_ERR_CUDA, err);
+    if ((e = launch_dist_put_V(Gv, d.n, k, kcmax, d.rows_max, d.pr, d.pc, bdev, Y, stream)))
+        return cuda_fail(e, "assemble Y");
+    return FFSPMV_OK;
 }
 
 ffspmv_status apply_op(ffspmv_matrix A, int which, uint32_t alpha, const uint32_t *x, uint64_t nx,
                        uint32_t beta, uint32_t *y, uint64_t ny, void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
-    if (A->dist) return no_dist(A);
+    if (A->dist) {
+        if (which != 0) return no_dist(A);
+        if (nx != A->dist->n || ny != A->dist->n)
+            return fail(FFSPMV_ERR_DIM, "x and y must have " + std::to_string(A->dist->n) + " entries");
+        if (A->dist->n && (!x || !y)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL vector");
+        if (overlaps(x, nx * 4, y, ny * 4)) return fail(FFSPMV_ERR_INVALID_ARG, "x overlaps y");
+        DeviceGuard guard(A->device);
+        return block_dist(A, 1, alpha, x, beta, y, stream);
+    }
     const bool scatter = which == 1 && !A->has_op[1] && !A->has_pan[1] && !A->has_run[1];
     if (scatter && !A->tacc) return fail(FFSPMV_ERR_UNSUPPORTED, "transpose not available");
     uint64_t orows, ocols;
@@ -863,9 +931,18 @@ ffspmv_status ffspmv_apply_block(ffspmv_matrix A, uint32_t k, uint32_t alpha, co
                                  uint64_t ldx, uint32_t beta, uint32_t *Y, uint64_t ldy,
                                  void *stream) {
     if (!A) return fail(FFSPMV_ERR_INVALID_ARG, "NULL handle");
-    if (A->dist) return no_dist(A);
     if (k == 0) return fail(FFSPMV_ERR_INVALID_ARG, "k must be >= 1");
     if (ldx < k || ldy < k) return fail(FFSPMV_ERR_INVALID_ARG, "leading dimension < k");
+    if (A->dist) {
+        const uint64_t n = A->dist->n;
+        if (ldx != k || ldy != k)
+            return fail(FFSPMV_ERR_UNSUPPORTED, "a distributed block apply needs ldx = ldy = k");
+        if (n && (!X || !Y)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL block");
+        if (overlaps(X, n * k * 4, Y, n * k * 4)) return fail(FFSPMV_ERR_INVALID_ARG, "X overlaps Y");
+        if (n * k >= (1ull << 32)) return fail(FFSPMV_ERR_DIM, "n * k must be < 2^32 elements");
+        DeviceGuard guard(A->device);
+        return block_dist(A, k, alpha, X, beta, Y, stream);
+    }
     const DevOp &op = A->op[0];
     if ((op.cols && !X) || (op.rows && !Y)) return fail(FFSPMV_ERR_INVALID_ARG, "NULL block");
     if (overlaps(X, op.cols * ldx * 4, Y, op.rows * ldy * 4))

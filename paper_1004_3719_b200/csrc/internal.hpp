@@ -341,6 +341,9 @@ int launch_sequence_dist(const DevOp &op, const DevMod &M, const uint32_t *X, ui
                          const DistSeq &d, void *stream);
 int launch_dist_sum_S(const uint32_t *G, uint64_t L, uint32_t ku, uint32_t k, uint32_t kcmax, uint32_t pr,
                       uint32_t pc, const DevMod &M, uint32_t *S, void *stream);
+// X (n x k, caller layout) -> columns [c0, c0 + kc) in the padded band layout
+int launch_dist_prep_x(const uint32_t *X, uint32_t k, uint32_t c0, uint32_t kc, uint64_t npad,
+                       uint32_t rows_max, const uint32_t *bstart_dev, uint32_t *Xp, void *stream);
 int launch_dist_put_V(const uint32_t *Gv, uint64_t n, uint32_t k, uint32_t kcmax, uint32_t rows_max,
                       uint32_t pr, uint32_t pc, const uint32_t *bstart_dev, uint32_t *V_out, void *stream);
 uint64_t kernel_launch_count();

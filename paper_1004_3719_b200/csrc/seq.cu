@@ -972,6 +972,15 @@ int launch_dist_sum_S(const uint32_t *G, uint64_t L, uint32_t ku, uint32_t k, ui
     return (int)cudaGetLastError();
 }
 
+int launch_dist_prep_x(const uint32_t *X, uint32_t k, uint32_t c0, uint32_t kc, uint64_t npad,
+                       uint32_t rows_max, const uint32_t *bstart_dev, uint32_t *Xp, void *stream) {
+    if (!npad || !kc) return 0;
+    k_dist_prep<uint32_t><<<(uint32_t)num_sms() * 8, 256, 0, (cudaStream_t)stream>>>(X, k, c0, kc, npad, rows_max,
+                                                                                    bstart_dev, Xp);
+    count_launch();
+    return (int)cudaGetLastError();
+}
+
 int launch_dist_put_V(const uint32_t *Gv, uint64_t n, uint32_t k, uint32_t kcmax, uint32_t rows_max,
                       uint32_t pr, uint32_t pc, const uint32_t *bstart_dev, uint32_t *V_out, void *stream) {
     const uint64_t total = n * k;

@@ -100,10 +100,74 @@ def test_dist_handle_rejects_other_ops(ff, cuda):
     A = ff.ffspmv_create(50, 50, ri, ci, val, m, comm=comms[0])
     x = torch.zeros(50, dtype=torch.int32, device="cuda")
     with pytest.raises(ff.FFSPMVError) as e:
-        ff.ffspmv_apply(A, 1, x, 0, torch.zeros(50, dtype=torch.int32, device="cuda"))
+        ff.ffspmv_apply_transpose(A, 1, x, 0, torch.zeros(50, dtype=torch.int32, device="cuda"))
+    assert e.value.status == ff.ERR_UNSUPPORTED
+    X = torch.zeros((50, 8), dtype=torch.int32, device="cuda")
+    Ypad = torch.zeros((50, 12), dtype=torch.int32, device="cuda")[:, :8]
+    with pytest.raises(ff.FFSPMVError) as e:              # distributed blocks are contiguous
+        ff.ffspmv_apply_block(A, 8, 1, X, 0, Ypad)
     assert e.value.status == ff.ERR_UNSUPPORTED
     with pytest.raises(ff.FFSPMVError) as e:
         ff.ffspmv_create(50, 60, ri, ci, val, m, comm=comms[0])
     assert e.value.status == ff.ERR_NONSQUARE
     del A
     comms[0].close()
+
+
+def _run_grid_block(ff, n, ri, ci, val, m, X, Y0, alpha, beta, pr, pc):
+    """Every rank runs Y <- alpha A X + beta Y (k = X.shape[1]; k = 1 through
+    ffspmv_apply) on a distributed handle with the replicated Y0."""
+    import torch
+    world = pr * pc
+    comms = ff.ffspmv_comm_create_local(world)
+    out, errs = [None] * world, [None] * world
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                A = ff.ffspmv_create(n, n, ri, ci, val, m, comm=comms[r], dist_rows=pr)
+                Xd = torch.from_numpy(np.ascontiguousarray(X).view(np.int32)).cuda()
+                Yd = torch.from_numpy(np.ascontiguousarray(Y0).view(np.int32)).cuda()
+                if X.shape[1] == 1:
+                    ff.ffspmv_apply(A, alpha, Xd.view(-1), beta, Yd.view(-1), stream=st)
+                else:
+                    ff.ffspmv_apply_block(A, X.shape[1], alpha, Xd, beta, Yd, stream=st)
+                st.synchronize()
+                out[r] = Yd.cpu().numpy().view(np.uint32)
+                del A
+        except Exception as e:            # reported by the main thread
+            errs[r] = e
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for c in comms:
+        c.close()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (2, 1), (1, 2), (2, 2), (3, 1), (4, 1)])
+@pytest.mark.parametrize("m", [3, 65521, (1 << 31) - 1])
+def test_dist_apply_block_grids(ff, oracle_mod, cuda, m, grid):
+    """Row-sharded single products on a distributed handle (each
+    rank its band x column block, then one all-gather): Y on every rank equals
+    the oracle's alpha A X + beta Y, for k = 1 (ffspmv_apply), a ragged k and
+    the vectorised widths."""
+    pr, pc = grid
+    g = synth.rng(31 * pr + 7 * pc + m % 97)
+    n = 650
+    ri, ci, val = synth.random_coo(g, n, n, 7 * n, m, dup=0.03)
+    for k in (1, 5, 8, 16):
+        X = synth.uniform(g, (n, k), m)
+        Y0 = synth.uniform(g, (n, k), m)
+        alpha, beta = int(g.integers(0, m)), int(g.integers(0, m))
+        want = oracle_mod.apply_block(n, n, ri, ci, val, m, X, Y0, alpha, beta)
+        for r, Y in enumerate(_run_grid_block(ff, n, ri, ci, val, m, X, Y0, alpha, beta, pr, pc)):
+            assert np.array_equal(Y.reshape(want.shape), want), (grid, k, r)

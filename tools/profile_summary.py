@@ -50,7 +50,7 @@ def main(src, dst):
     tot = sum(a[1] for a in agg.values())
     md += ["## Launch list of `python bench.py --steps 3 --warmup 3` under ncu", "",
            f"{len(L)} launches, {tot / 1e6:.2f} ms of kernel time in total (all phases of the bench:",
-           "headline c2 apply/transpose, e2e, and the c3/c4/c5 extras).", "",
+           "headline c3 apply, e2e, the cpu baseline, and the c2/c4/c5/c3sq extras).", "",
            "| kernel | launches | total µs | share | µs/launch |", "|---|---:|---:|---:|---:|"]
     for k, (n, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:20]:
         md.append(f"| `{k[:70]}` | {n} | {ns / 1e3:.1f} | {100 * ns / tot:.1f}% | {ns / n / 1e3:.1f} |")
