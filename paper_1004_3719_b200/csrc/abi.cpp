@@ -783,7 +783,8 @@ ffspmv_status block_dist(ffspmv_matrix A, uint32_t k, uint32_t alpha, const uint
             return cuda_fail(e, "scatter X");
         if (h && (e = launch_block(op, A->mod, kc, alpha, Xp, kc, beta, Y + row0 * k + c0, k, stream)))
             return cuda_fail(e, "band block apply");
-        if (h && (e = cudaMemcpy2DAsync(Vb, kcmax * 4ull, Y + row0 * k + c0, k * 4ull, kc * 4ull, h,
+        // packed with the block's own width (k_dist_put_V's slot layout)
+        if (h && (e = cudaMemcpy2DAsync(Vb, kc * 4ull, Y + row0 * k + c0, k * 4ull, kc * 4ull, h,
                                         cudaMemcpyDeviceToDevice, st)))
             return cuda_fail(e, "pack band block");
     }

@@ -1,6 +1,7 @@
 """One-rank NCCL run of bench._seq_dist at full c5 size: the N > 1 sequence
 line's code path (C-ABI distributed handle, NCCL communicator, per-step
-ncclAllGather) measured on a one-GPU box (grid 1 x 1)."""
+ncclAllGather) measured on a one-GPU box (grid 1 x 1), and the row-sharded
+c4 block apply line (bench._block_dist) the same way."""
 import json
 import os
 import sys
@@ -20,5 +21,7 @@ import paper_1004_3719_b200 as ff
 
 ff.load()
 args = types.SimpleNamespace(steps=int(os.environ.get("STEPS", "40")), warmup=4)
+args.no_extras = False
 print(json.dumps(bench._seq_dist(args, 1, 0, 0)))
+print(json.dumps(bench._block_dist(args, 1)))
 dist.destroy_process_group()
