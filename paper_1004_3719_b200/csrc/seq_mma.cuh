@@ -28,6 +28,9 @@ namespace ffspmv {
 constexpr int SMMA_WARPS = 8;
 constexpr int SMMA_KMAX = 16;     // iterate columns handled by the fused kernel (k <= 16)
 constexpr int SMMA_FOLD = 512;    // slices between s32 -> u64 folds
+// byte stride of the hi / lo planes of the transposed limb tile VT[plane][col][row]
+// in the k <= 16 half-slice kernels (k_seq_step_h)
+constexpr int SEQ_VT_PLANE = SMMA_KMAX * 32;
 
 // NR consecutive rows x 4 columns per lane: KPV = k/4 lanes per row (1, 2,
 // 4), G = 32/KPV row groups, group g owns rows NR*g .. NR*g+NR-1, so a lane's
@@ -393,7 +396,7 @@ __device__ __forceinline__ void seq_slice_h(const DevOp &op, const DevMod &M, ui
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 vt[(c0 + i) * 32 + rl] = (uint8_t)(r[i] >> 8);
-                vt[32 * 32 + (c0 + i) * 32 + rl] = (uint8_t)r[i];
+                vt[SEQ_VT_PLANE + (c0 + i) * 32 + rl] = (uint8_t)r[i];
             }
         }
     }
@@ -411,7 +414,7 @@ __device__ __forceinline__ void seq_slice_h(const DevOp &op, const DevMod &M, ui
         for (int jj = 0; jj < 2; ++jj) {
             const uint32_t off = b * 32 + tig * 4 + 16 * jj;
             bh[jj] = *reinterpret_cast<const uint32_t *>(vt + off);
-            bl[jj] = *reinterpret_cast<const uint32_t *>(vt + 32 * 32 + off);
+            bl[jj] = *reinterpret_cast<const uint32_t *>(vt + SEQ_VT_PLANE + off);
         }
         int hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
         mma_u8(hh, ah, bh);
@@ -438,6 +441,9 @@ __device__ __forceinline__ void seq_slice_h(const DevOp &op, const DevMod &M, ui
 // seq_slice_h.
 #ifndef FFSPMV_SEQ_AS_D
 #define FFSPMV_SEQ_AS_D 2
+#endif
+#ifndef FFSPMV_SEQ_A64
+#define FFSPMV_SEQ_A64 0
 #endif
 template <int LPR>
 struct SeqRing {
@@ -472,12 +478,20 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
     const unsigned char *vbl = reinterpret_cast<const unsigned char *>(op.vval) +
                                ((uint64_t)h.off_v - wp * 32) * sizeof(VT) + lane * 4;
     const bool vlane = lane < 8 * sizeof(VT);
-    uint32_t a32[NR][8];
+    // +-1 addends in u32 (a -1 adds m - x: < 2^32 for <= 65535 entries) and
+    // valued products in u64; FFSPMV_SEQ_A64 keeps both in the u64 (16 fewer
+    // registers for NR = 2, one more instruction per +-1 addend)
+#if FFSPMV_SEQ_A64
+    constexpr int A32N = 1;
+#else
+    constexpr int A32N = NR;
+#endif
+    uint32_t a32[A32N][8];
     unsigned long long a64[NR][8];
 #pragma unroll
     for (int i = 0; i < NR; ++i)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) { a32[i][c] = 0; a64[i][c] = 0; }
+        for (int c = 0; c < 8; ++c) { a64[i][c] = 0; if (i < A32N) a32[i][c] = 0; }
     auto copy_idx = [&](uint32_t j) {
         const uint32_t q = (j & (2 * D - 1)) * 128;
         cp_async4(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
@@ -506,8 +520,13 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
                 const uint32_t sm = (uint32_t)((int32_t)iw[q * 32 + r] >> 31), sa = sm & (m + 1);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
+#if FFSPMV_SEQ_A64
+                    a64[i][2 * c] += ((xs[c] & 0xFFFFu) ^ sm) + sa;
+                    a64[i][2 * c + 1] += ((xs[c] >> 16) ^ sm) + sa;
+#else
                     a32[i][2 * c] += ((xs[c] & 0xFFFFu) ^ sm) + sa;
                     a32[i][2 * c + 1] += ((xs[c] >> 16) ^ sm) + sa;
+#endif
                 }
             } else {
                 const uint32_t a = reinterpret_cast<const VT *>(iv + q * 128)[r];
@@ -558,7 +577,7 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
         const uint32_t rl = i * RPP + g;
         uint32_t r[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) r[c] = mod48(a64[i][c] + a32[i][c], M);
+        for (int c = 0; c < 8; ++c) r[c] = mod48(a64[i][c] + (FFSPMV_SEQ_A64 ? 0u : a32[i < A32N ? i : 0][c]), M);
         if (rl >= h.nrows) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) r[c] = 0;
@@ -571,7 +590,7 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 vt[(c0 + c) * 32 + rl] = (uint8_t)(r[c] >> 8);
-                vt[32 * 32 + (c0 + c) * 32 + rl] = (uint8_t)r[c];
+                vt[SEQ_VT_PLANE + (c0 + c) * 32 + rl] = (uint8_t)r[c];
             }
         }
     }
@@ -588,7 +607,7 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
         for (int jj = 0; jj < 2; ++jj) {
             const uint32_t off = b * 32 + tig * 4 + 16 * jj;
             bh[jj] = *reinterpret_cast<const uint32_t *>(vt + off);
-            bl[jj] = *reinterpret_cast<const uint32_t *>(vt + 32 * 32 + off);
+            bl[jj] = *reinterpret_cast<const uint32_t *>(vt + SEQ_VT_PLANE + off);
         }
         int hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
         mma_u8(hh, ah, bh);
@@ -630,10 +649,20 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
              const uint32_t *__restrict__ ufrag, uint32_t *__restrict__ part_out,
              const uint32_t *__restrict__ part_prev, uint32_t nprev, uint32_t *__restrict__ S_prev,
              uint32_t *__restrict__ ctr, uint32_t *__restrict__ ctr_next) {
-    __shared__ __align__(16) uint8_t vts[SMMA_WARPS][2 * 32 * 32];
+    __shared__ __align__(16) uint8_t vts[SMMA_WARPS][2 * SEQ_VT_PLANE];
     __shared__ unsigned long long pn[16 * SMMA_KMAX];
     __shared__ unsigned long long p64s[SMMA_WARPS][SMMA_P64];
-    __shared__ uint32_t red[SMMA_WARPS][16][SMMA_KMAX];
+    extern __shared__ __align__(16) unsigned char seq_ring[];
+    // the CTA's final reduction tile: aliases each warp's own ring (idle once
+    // the warp has no items left) on the cp.async path
+    typedef uint32_t RedTile[16][SMMA_KMAX];
+    static_assert(sizeof(RedTile) <= SeqRing<1>::bytes, "reduction tile fits a warp's ring");
+#if FFSPMV_SEQ_AS
+    auto red = [&](uint32_t w) -> RedTile & { return *reinterpret_cast<RedTile *>(seq_ring + w * SeqRing<LPR>::bytes); };
+#else
+    __shared__ RedTile red_s[SMMA_WARPS];
+    auto red = [&](uint32_t w) -> RedTile & { return red_s[w]; };
+#endif
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
     const uint32_t pairs = ku * k;
@@ -665,7 +694,6 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
             const uint32_t s = w - op.n_long;
             const SliceHdr h = load_hdr_b(op.slices + s);
             if constexpr (FFSPMV_SEQ_AS) {
-                extern __shared__ __align__(16) unsigned char seq_ring[];
                 seq_slice_as<VT, LPR>(op, M, s, h, lane, k, Vin, Vout, ufrag, vts[warp], p64,
                                       seq_ring + warp * SeqRing<LPR>::bytes);
             } else {
@@ -682,7 +710,7 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t a = gid + 8 * (e >> 1), b = nt * 8 + tig * 2 + (e & 1);
-            red[warp][a][b] = mod64(p64[(nt * 4 + e) * 32 + lane], M);
+            red(warp)[a][b] = mod64(p64[(nt * 4 + e) * 32 + lane], M);
         }
     }
     __syncthreads();
@@ -690,7 +718,7 @@ k_seq_step_h(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
         const uint32_t a = i / k, b = i - a * k;
         uint64_t sacc = mod64(pn[a * k + b], M);
 #pragma unroll
-        for (int w = 0; w < SMMA_WARPS; ++w) sacc += red[w][a][b];
+        for (int w = 0; w < SMMA_WARPS; ++w) sacc += red(w)[a][b];
         part_out[(uint64_t)blockIdx.x * pairs + i] = mod64(sacc, M);
     }
 }
