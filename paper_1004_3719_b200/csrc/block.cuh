@@ -22,6 +22,12 @@
 
 #include "device.cuh"
 
+// 1: the cp.async walks' matrix-stream copies and the block output stores
+// carry L2 evict-first hints (0: no hints, A/B measurement)
+#ifndef FFSPMV_AS_HINT
+#define FFSPMV_AS_HINT 1
+#endif
+
 namespace ffspmv {
 
 void count_launch();
@@ -52,6 +58,28 @@ struct BlockOut {
     __device__ __forceinline__ void zero(uint32_t row, uint32_t col, const DevMod &M) {
         TY *p = Y + (uint64_t)row * ldy + col;
         *p = (TY)(beta ? mod64((uint64_t)beta * (uint32_t)*p, M) : 0u);
+    }
+    // columns col .. col + 3 (all valid when colok: k % 4 == 0); u32 blocks
+    // with beta = 0 leave as one 16-byte store, evict-first in L2 (the output
+    // is not re-read by this launch, the gathered X is)
+    // (HINT = false: plain stores -- measured faster for the two-pass k = 32
+    // walk, 258 vs 274 us on c4)
+    template <bool HINT>
+    __device__ __forceinline__ void put4(uint32_t row, uint32_t col, bool colok, const uint32_t (&r)[4],
+                                         const DevMod &M) {
+        if (!colok) return;
+        TY *p = Y + (uint64_t)row * ldy + col;
+        if constexpr (sizeof(TY) == 4 && HINT && FFSPMV_AS_HINT) {
+            if (!beta && ((uintptr_t)p & 15) == 0) {
+                const uint32_t a0 = epilogue(r[0], alpha, 0u, 0u, M), a1 = epilogue(r[1], alpha, 0u, 0u, M),
+                               a2 = epilogue(r[2], alpha, 0u, 0u, M), a3 = epilogue(r[3], alpha, 0u, 0u, M);
+                asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;"
+                             ::"l"(p), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "l"(POLICY_EVICT_FIRST) : "memory");
+                return;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) p[c] = (TY)epilogue(r[c], alpha, beta, beta ? (uint32_t)p[c] : 0u, M);
     }
 };
 
@@ -326,8 +354,16 @@ struct AsRing {
     static constexpr uint32_t bytes = data_bytes + 2 * D * 128 * 2;
 };
 
+// index words / values of the matrix stream: read once, evict first from L2
+// so the gathered X / V_t rows keep the cache (FFSPMV_AS_HINT = 0: no hint)
+// (HINT = false when the walk re-reads the stream: several passes per slice)
+template <bool HINT = true>
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint32_t n) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+    if constexpr (FFSPMV_AS_HINT && HINT)
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;"
+                     ::"r"(dst), "l"(src), "r"(n), "l"(POLICY_EVICT_FIRST) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
 }
 template <int BYTES>
 __device__ __forceinline__ void cp_async_v(uint32_t dst, const void *src, uint32_t n) {
@@ -376,8 +412,9 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
             // (j mod 2D), its rows into data ring (j mod D)
             auto copy_idx = [&](uint32_t j) {
                 const uint32_t q = (j & (2 * D - 1)) * 128;
-                cp_async4(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
-                if (j >= wp && vlane) cp_async4(siv + q + lane * 4, vbl + (uint64_t)j * 32 * sizeof(VT), 4);
+                constexpr bool once = PASSES == 1;   // the stream is read once per column chunk
+                cp_async4<once>(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
+                if (j >= wp && vlane) cp_async4<once>(siv + q + lane * 4, vbl + (uint64_t)j * 32 * sizeof(VT), 4);
             };
             auto copy_data = [&](uint32_t j) {
                 const uint32_t *w = iw + (j & (2 * D - 1)) * 32 + rbase;
@@ -473,8 +510,10 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
                 const uint32_t r = rbase + i * G;
                 if (r < h.nrows) {
                     const uint32_t row = op.perm[s * 32 + r];
+                    uint32_t res[CPL];
 #pragma unroll
-                    for (int c = 0; c < CPL; ++c) out.put(row, col + c, colok, acc[i][c].reduce(M), M);
+                    for (int c = 0; c < CPL; ++c) res[c] = acc[i][c].reduce(M);
+                    out.template put4<PASSES == 1>(row, col, colok, res, M);
                 }
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");
