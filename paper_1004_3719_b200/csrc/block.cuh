@@ -427,7 +427,10 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
                 }
             };
             Acc acc[NR][CPL];
-            auto consume = [&](uint32_t j) {
+            // KIND: 0 = +-1 slot, 1 = valued slot, 2 = decided by j < wp (the
+            // steady loops are split at wp so their consume has no branch)
+            auto consume = [&](uint32_t j, auto kind) {
+                constexpr int KIND = decltype(kind)::value;
                 const uint4 *d = data + (j & (D - 1)) * (NR * 32);
                 const uint32_t q = j & (2 * D - 1);
 #pragma unroll
@@ -446,7 +449,7 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
                         for (int c = 0; c < CPL; ++c) xs[c] = (xv[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
                     }
                     const uint32_t r = rbase + i * G;
-                    if (j < wp) {
+                    if (KIND == 0 || (KIND == 2 && j < wp)) {
                         // -1: (x ^ ~0) + (m + 1) = m - x (mod 2^32)
                         const uint32_t sm = (uint32_t)((int32_t)iw[q * 32 + r] >> 31), sa = sm & (m + 1);
 #pragma unroll
@@ -458,6 +461,9 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
                     }
                 }
             };
+            using PM = std::integral_constant<int, 0>;
+            using VAL = std::integral_constant<int, 1>;
+            using ANY = std::integral_constant<int, 2>;
             auto wait_sync = [&]() {
                 asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
                 __syncwarp();
@@ -486,10 +492,25 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
             }
             // steady state: consume j, gathers of j + D, index words of j + 2D
             uint32_t j = 0;
+            // split at wp for KPV >= 4 (A/B on one box: c4 k = 16 / 32 147 -> 129
+            // us, 258 -> 244 us; k = 8 86 -> 96 us, so KPV = 2 keeps one loop)
+            constexpr bool SPLIT = KPV >= 4;
+            const uint32_t jend = wt > 2 * D ? wt - 2 * D : 0, jpm = SPLIT ? min(wp, jend) : 0;
 #pragma unroll 1
-            for (; j + 2 * D < wt; ++j) {
+            for (; j < jpm; ++j) {
                 wait_sync();
-                consume(j);
+                consume(j, PM());
+                maybe_fold();
+                __syncwarp();
+                copy_idx(j + 2 * D);
+                copy_data(j + D);
+                commit();
+            }
+#pragma unroll 1
+            for (; j < jend; ++j) {
+                wait_sync();
+                if constexpr (SPLIT) consume(j, VAL());
+                else consume(j, ANY());
                 maybe_fold();
                 __syncwarp();
                 copy_idx(j + 2 * D);
@@ -499,7 +520,7 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
 #pragma unroll 1
             for (; j < wt; ++j) {
                 wait_sync();
-                consume(j);
+                consume(j, ANY());
                 maybe_fold();
                 __syncwarp();
                 if (j + D < wt) copy_data(j + D);
