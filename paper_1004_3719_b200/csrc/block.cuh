@@ -375,6 +375,35 @@ __device__ __forceinline__ void cp_async_v(uint32_t dst, const void *src, uint32
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
 }
 
+// N consecutive naturally aligned shared elements of type T (N * sizeof(T)
+// <= 16 bytes) with one vector load, widened to u32: a lane's NR index words
+// or values in the rings (lanes own consecutive rows, see block_slice_as).
+template <class T, int N>
+__device__ __forceinline__ void lds_vec(const void *p, uint32_t (&v)[N]) {
+    constexpr int B = N * (int)sizeof(T);
+    static_assert(B == 1 || B == 2 || B == 4 || B == 8 || B == 16, "vector width");
+    uint32_t u[4] = {0, 0, 0, 0};
+    if constexpr (B == 16) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(p);
+        u[0] = q.x; u[1] = q.y; u[2] = q.z; u[3] = q.w;
+    } else if constexpr (B == 8) {
+        const uint2 q = *reinterpret_cast<const uint2 *>(p);
+        u[0] = q.x; u[1] = q.y;
+    } else if constexpr (B == 4) {
+        u[0] = *reinterpret_cast<const uint32_t *>(p);
+    } else if constexpr (B == 2) {
+        u[0] = *reinterpret_cast<const uint16_t *>(p);
+    } else {
+        u[0] = *reinterpret_cast<const uint8_t *>(p);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        if constexpr (sizeof(T) == 4) v[i] = u[i];
+        else if constexpr (sizeof(T) == 2) v[i] = (u[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+        else v[i] = (u[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+    }
+}
+
 template <class Acc, class VT, int KPV, int NR, int D, class TX, class Out>
 __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M, uint32_t s,
                                                const SliceHdr &h, uint32_t lane, uint32_t k,
@@ -407,7 +436,9 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
         const TX *Xc = X + col;
 #pragma unroll 1
         for (int pass = 0; pass < PASSES; ++pass) {
-            const uint32_t rbase = pass * G * NR + g;
+            // a lane's NR rows of this pass are consecutive (rbase .. rbase +
+            // NR - 1), so their index words / values come with one vector load
+            const uint32_t rbase = pass * G * NR + g * NR;
             // copies of slot j: its index word / value bytes into idx ring
             // (j mod 2D), its rows into data ring (j mod D)
             auto copy_idx = [&](uint32_t j) {
@@ -417,11 +448,12 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
                 if (j >= wp && vlane) cp_async4<once>(siv + q + lane * 4, vbl + (uint64_t)j * 32 * sizeof(VT), 4);
             };
             auto copy_data = [&](uint32_t j) {
-                const uint32_t *w = iw + (j & (2 * D - 1)) * 32 + rbase;
+                uint32_t w[NR];
+                lds_vec<uint32_t, NR>(iw + (j & (2 * D - 1)) * 32 + rbase, w);
                 const uint32_t dst = sdata + (j & (D - 1)) * (NR * 512);
 #pragma unroll
                 for (int i = 0; i < NR; ++i) {
-                    const uint32_t c = w[i * G];
+                    const uint32_t c = w[i];
                     const bool ok = c != PAD_COL && colok;
                     cp_async_v<BYTES>(dst + i * 512, Xc + (ok ? (c & COL_MASK) * ldx : 0u), ok ? BYTES : 0);
                 }
@@ -433,6 +465,9 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
                 constexpr int KIND = decltype(kind)::value;
                 const uint4 *d = data + (j & (D - 1)) * (NR * 32);
                 const uint32_t q = j & (2 * D - 1);
+                uint32_t wa[NR];     // the rows' index words (+-1: sign) or values
+                if (KIND == 0 || (KIND == 2 && j < wp)) lds_vec<uint32_t, NR>(iw + q * 32 + rbase, wa);
+                else lds_vec<VT, NR>(iv + q * 128 + rbase * sizeof(VT), wa);
 #pragma unroll
                 for (int i = 0; i < NR; ++i) {
                     const uint4 v = d[i * 32];
@@ -448,16 +483,14 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
 #pragma unroll
                         for (int c = 0; c < CPL; ++c) xs[c] = (xv[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
                     }
-                    const uint32_t r = rbase + i * G;
                     if (KIND == 0 || (KIND == 2 && j < wp)) {
                         // -1: (x ^ ~0) + (m + 1) = m - x (mod 2^32)
-                        const uint32_t sm = (uint32_t)((int32_t)iw[q * 32 + r] >> 31), sa = sm & (m + 1);
+                        const uint32_t sm = (uint32_t)((int32_t)wa[i] >> 31), sa = sm & (m + 1);
 #pragma unroll
                         for (int c = 0; c < CPL; ++c) acc[i][c].add((xs[c] ^ sm) + sa);
                     } else {
-                        const uint32_t a = reinterpret_cast<const VT *>(iv + q * 128)[r];
 #pragma unroll
-                        for (int c = 0; c < CPL; ++c) acc[i][c].mad(a, xs[c]);
+                        for (int c = 0; c < CPL; ++c) acc[i][c].mad(wa[i], xs[c]);
                     }
                 }
             };
@@ -495,9 +528,9 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
             // split at wp for KPV >= 4 (A/B on one box: c4 k = 16 / 32 147 -> 129
             // us, 258 -> 244 us; k = 8 86 -> 96 us, so KPV = 2 keeps one loop)
             constexpr bool SPLIT = KPV >= 4;
-            const uint32_t jend = wt > 2 * D ? wt - 2 * D : 0, jpm = SPLIT ? min(wp, jend) : 0;
+            const uint32_t jend = wt > 2 * D ? wt - 2 * D : 0, jpm = SPLIT ? min(wp, jend) : 0u;
 #pragma unroll 1
-            for (; j < jpm; ++j) {
+            for (; SPLIT && j < jpm; ++j) {
                 wait_sync();
                 consume(j, PM());
                 maybe_fold();
@@ -528,7 +561,7 @@ __device__ __forceinline__ void block_slice_as(const DevOp &op, const DevMod &M,
             }
 #pragma unroll
             for (int i = 0; i < NR; ++i) {
-                const uint32_t r = rbase + i * G;
+                const uint32_t r = rbase + i;
                 if (r < h.nrows) {
                     const uint32_t row = op.perm[s * 32 + r];
                     uint32_t res[CPL];

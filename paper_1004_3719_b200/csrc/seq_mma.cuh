@@ -461,7 +461,6 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
                                              unsigned long long *p64, unsigned char *ring) {
     constexpr int D = SeqRing<LPR>::D;
     constexpr int NR = LPR;                 // rows per lane (one pass over the slice)
-    constexpr uint32_t RPP = 32 / LPR;      // rows per lane group
     static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(ring);
     const uint32_t sdata = sbase + lane * 16;
@@ -497,12 +496,15 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
         cp_async4(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
         if (j >= wp && vlane) cp_async4(siv + q + lane * 4, vbl + (uint64_t)j * 32 * sizeof(VT), 4);
     };
+    // a lane's NR rows are consecutive (g NR .. g NR + NR - 1): one vector
+    // load of their index words / values per slot
     auto copy_data = [&](uint32_t j) {
-        const uint32_t *w = iw + (j & (2 * D - 1)) * 32 + g;
+        uint32_t w[NR];
+        lds_vec<uint32_t, NR>(iw + (j & (2 * D - 1)) * 32 + g * NR, w);
         const uint32_t dst = sdata + (j & (D - 1)) * (NR * 512);
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
-            const uint32_t c = w[i * RPP];
+            const uint32_t c = w[i];
             const bool ok = c != PAD_COL && colok;
             cp_async_v<16>(dst + i * 512, Vc + (ok ? (c & COL_MASK) * k : 0u), ok ? 16u : 0u);
         }
@@ -512,14 +514,16 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
         constexpr int KIND = decltype(kind)::value;
         const uint4 *d = data + (j & (D - 1)) * (NR * 32);
         const uint32_t q = j & (2 * D - 1);
+        uint32_t wa[NR];     // the rows' index words (+-1: sign) or values
+        if (KIND == 0 || (KIND == 2 && j < wp)) lds_vec<uint32_t, NR>(iw + q * 32 + g * NR, wa);
+        else lds_vec<VT, NR>(iv + q * 128 + g * NR * sizeof(VT), wa);
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
             const uint4 v = d[i * 32];
             const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
-            const uint32_t r = i * RPP + g;
             if (KIND == 0 || (KIND == 2 && j < wp)) {
                 // -1: (x ^ ~0) + (m + 1) = m - x (mod 2^32)
-                const uint32_t sm = (uint32_t)((int32_t)iw[q * 32 + r] >> 31), sa = sm & (m + 1);
+                const uint32_t sm = (uint32_t)((int32_t)wa[i] >> 31), sa = sm & (m + 1);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
 #if FFSPMV_SEQ_A64
@@ -531,7 +535,7 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
 #endif
                 }
             } else {
-                const uint32_t a = reinterpret_cast<const VT *>(iv + q * 128)[r];
+                const uint32_t a = wa[i];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     a64[i][2 * c] += (unsigned long long)a * (xs[c] & 0xFFFFu);
@@ -560,9 +564,9 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
     // split at wp for k = 16 (c5: 0.225 -> 0.215 ms/step); k = 8 keeps one
     // loop (the 4-column block walk with two lanes per row was slower split)
     constexpr bool SPLIT = LPR >= 2;
-    const uint32_t jend = wt > 2 * D ? wt - 2 * D : 0, jpm = SPLIT ? min(wp, jend) : 0;
+    const uint32_t jend = wt > 2 * D ? wt - 2 * D : 0, jpm = SPLIT ? min(wp, jend) : 0u;
 #pragma unroll 1
-    for (; j < jpm; ++j) {
+    for (; SPLIT && j < jpm; ++j) {
         wait_sync();
         consume(j, PM());
         __syncwarp();
@@ -593,7 +597,7 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
     // residues -> V_{t+1} and the transposed limb tile (as seq_slice_h)
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
-        const uint32_t rl = i * RPP + g;
+        const uint32_t rl = g * NR + i;
         uint32_t r[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) r[c] = mod48(a64[i][c] + (FFSPMV_SEQ_A64 ? 0u : a32[i < A32N ? i : 0][c]), M);
