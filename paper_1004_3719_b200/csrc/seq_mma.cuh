@@ -491,6 +491,11 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
     for (int i = 0; i < NR; ++i)
 #pragma unroll
         for (int c = 0; c < 8; ++c) { a64[i][c] = 0; if (i < A32N) a32[i][c] = 0; }
+    // loaded now, used after the slot walk (its latency hides behind it)
+    uint32_t prow[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) prow[i] = g * NR + i < h.nrows ? __ldg(op.perm + s * 32 + g * NR + i) : 0u;
+
     auto copy_idx = [&](uint32_t j) {
         const uint32_t q = (j & (2 * D - 1)) * 128;
         cp_async4(siw + q + lane * 4, j < wp ? pcl + j * 32 : vcl + j * 32, 4);
@@ -594,32 +599,46 @@ __device__ __forceinline__ void seq_slice_as(const DevOp &op, const DevMod &M, u
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-    // residues -> V_{t+1} and the transposed limb tile (as seq_slice_h)
+    // U fragments of the slice: loaded before the residue arithmetic they wait behind
+    const uint4 ah4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256) + lane);
+    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
+    // residues -> V_{t+1} and the transposed limb tile (as seq_slice_h); the
+    // lane's NR rows are adjacent in the tile, so NR = 2 writes both rows'
+    // bytes of a column with one 16-bit store per plane
+    uint32_t r[NR][8];
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
         const uint32_t rl = g * NR + i;
-        uint32_t r[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) r[c] = mod48(a64[i][c] + (FFSPMV_SEQ_A64 ? 0u : a32[i < A32N ? i : 0][c]), M);
+        for (int c = 0; c < 8; ++c) r[i][c] = mod48(a64[i][c] + (FFSPMV_SEQ_A64 ? 0u : a32[i < A32N ? i : 0][c]), M);
         if (rl >= h.nrows) {
 #pragma unroll
-            for (int c = 0; c < 8; ++c) r[c] = 0;
+            for (int c = 0; c < 8; ++c) r[i][c] = 0;
         } else if (colok) {
-            const uint32_t row = op.perm[s * 32 + rl];
-            *reinterpret_cast<uint4 *>(Vout + (uint64_t)row * k + c0) =
-                make_uint4(r[0] | r[1] << 16, r[2] | r[3] << 16, r[4] | r[5] << 16, r[6] | r[7] << 16);
+            *reinterpret_cast<uint4 *>(Vout + (uint64_t)prow[i] * k + c0) =
+                make_uint4(r[i][0] | r[i][1] << 16, r[i][2] | r[i][3] << 16, r[i][4] | r[i][5] << 16,
+                           r[i][6] | r[i][7] << 16);
         }
-        if (colok) {
+    }
+    if (colok) {
+        if constexpr (NR == 2) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                vt[(c0 + c) * 32 + rl] = (uint8_t)(r[c] >> 8);
-                vt[SEQ_VT_PLANE + (c0 + c) * 32 + rl] = (uint8_t)r[c];
+                const uint32_t off = (c0 + c) * 32 + g * 2;
+                *reinterpret_cast<uint16_t *>(vt + off) = (uint16_t)((r[0][c] >> 8) | (r[1][c] & 0xFF00u));
+                *reinterpret_cast<uint16_t *>(vt + SEQ_VT_PLANE + off) = (uint16_t)((r[0][c] & 0xFFu) | (r[1][c] & 0xFFu) << 8);
             }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NR; ++i)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    vt[(c0 + c) * 32 + g * NR + i] = (uint8_t)(r[i][c] >> 8);
+                    vt[SEQ_VT_PLANE + (c0 + c) * 32 + g * NR + i] = (uint8_t)r[i][c];
+                }
         }
     }
     __syncwarp();
-    const uint4 ah4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256) + lane);
-    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
     const uint32_t ah[4] = {ah4.x, ah4.y, ah4.z, ah4.w}, al[4] = {al4.x, al4.y, al4.z, al4.w};
     const uint32_t gid = lane >> 2, tig = lane & 3;
 #pragma unroll
