@@ -796,6 +796,9 @@ __device__ __forceinline__ void seq_slice_b(const DevOp &op, const DevMod &M, ui
     uint32_t acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0;
+    // the output row and the U fragments, loaded now and used after the walk
+    const uint32_t prow = lane < h.nrows ? __ldg(op.perm + s * 32 + lane) : 0u;
+    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
     // +-1 slots: x, or m - x for a -1: (x ^ ~0) + (m + 1) = m - x (mod 2^32)
     {
         uint32_t c = wp ? ld_bcast(pc) : PAD_COL;
@@ -840,7 +843,7 @@ __device__ __forceinline__ void seq_slice_b(const DevOp &op, const DevMod &M, ui
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = 0;
     } else {
-        const uint32_t row = op.perm[s * 32 + lane];
+        const uint32_t row = prow;
         uint32_t w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) w[q] = r[4 * q] | r[4 * q + 1] << 8 | r[4 * q + 2] << 16 | r[4 * q + 3] << 24;
@@ -850,7 +853,6 @@ __device__ __forceinline__ void seq_slice_b(const DevOp &op, const DevMod &M, ui
     for (int i = 0; i < 16; ++i) vt[i * 32 + lane] = (uint8_t)r[i];
     __syncwarp();
     // projection: U^T V with single-limb residues (the U fragments' low plane)
-    const uint4 al4 = __ldg(reinterpret_cast<const uint4 *>(ufrag + (uint64_t)s * 256 + 128) + lane);
     const uint32_t al[4] = {al4.x, al4.y, al4.z, al4.w};
     const uint32_t gid = lane >> 2, tig = lane & 3;
 #pragma unroll
@@ -1028,7 +1030,11 @@ k_seq_step_b(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
     __shared__ __align__(16) uint8_t vts[SMMA_WARPS][32 * 32];
     __shared__ unsigned long long pn[16 * SMMA_KMAX];
     __shared__ unsigned long long p64s[SMMA_WARPS][SMMA_P64];
-    __shared__ uint32_t red[SMMA_WARPS][16][SMMA_KMAX];
+    // the CTA's final reduction tile of warp w aliases w's own p64 block
+    // (its values are read into registers first): 8 KB less static shared
+    typedef uint32_t RedTile[16][SMMA_KMAX];
+    static_assert(sizeof(RedTile) <= sizeof(p64s[0]), "reduction tile fits a warp's p64 block");
+    auto red = [&](uint32_t w) -> RedTile & { return *reinterpret_cast<RedTile *>(&p64s[w][0]); };
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t gw = blockIdx.x * SMMA_WARPS + warp, nw = gridDim.x * SMMA_WARPS;
     const uint32_t pairs = ku * k;
@@ -1072,12 +1078,18 @@ k_seq_step_b(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
         w = __shfl_sync(0xFFFFFFFFu, wn, 0);
     }
     const uint32_t gid = lane >> 2, tig = lane & 3;
+    uint32_t pr[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pr[nt][e] = mod64(p64[(nt * 4 + e) * 32 + lane], M);
+    __syncwarp();
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t a = gid + 8 * (e >> 1), b = nt * 8 + tig * 2 + (e & 1);
-            red[warp][a][b] = mod64(p64[(nt * 4 + e) * 32 + lane], M);
+            red(warp)[a][b] = pr[nt][e];
         }
     }
     __syncthreads();
@@ -1085,7 +1097,7 @@ k_seq_step_b(DevOp op, const DevOp *__restrict__ opdev, DevMod M, uint32_t k, ui
         const uint32_t a = i / k, b = i - a * k;
         uint64_t sacc = mod64(pn[a * k + b], M);
 #pragma unroll
-        for (int w = 0; w < SMMA_WARPS; ++w) sacc += red[w][a][b];
+        for (int w = 0; w < SMMA_WARPS; ++w) sacc += red(w)[a][b];
         part_out[(uint64_t)blockIdx.x * pairs + i] = mod64(sacc, M);
     }
 }
